@@ -1,0 +1,172 @@
+/*
+ * gss.h — C ABI of the B200-native survival-scan (Cox / Fine-Gray CCD) engine.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and int status codes,
+ * no C++ or torch types.  It flattens the reference's C++ `survscan::Engine`
+ * surface (/root/reference/proj/include/survscan/engine.hpp:33-90) and the
+ * CCD driver (include/survscan/ccd.hpp:59-72) so any host language can bind
+ * it; the repo's own C++ mirror of the reference API
+ * (paper_2204_08183_b200/csrc/host/) and its pybind module sit on top.
+ * INTEGRATION.md shows the ctypes / C++ bindings a maintainer would add.
+ *
+ * Threading: calls on DISTINCT engine handles are thread-safe; one handle
+ * must not be used by two threads at once (engine.hpp:29-32).  Each engine
+ * owns one CUDA stream.  Errors are returned as status codes (one per
+ * reference exception class, include/survscan/errors.hpp:9-65) and the
+ * message of the last failure on the calling thread is gss_last_error().
+ */
+#ifndef GSS_H
+#define GSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1:1 with survscan::Error subclasses (errors.hpp) ---- */
+enum gss_status {
+  GSS_OK = 0,
+  GSS_ERR_PARSE = 1,           /* ParseError               errors.hpp:17 */
+  GSS_ERR_SCHEMA = 2,          /* SchemaError              errors.hpp:22 */
+  GSS_ERR_DOMAIN = 3,          /* DomainError              errors.hpp:27 */
+  GSS_ERR_INDEX = 4,           /* IndexError               errors.hpp:32 */
+  GSS_ERR_DUPLICATE = 5,       /* DuplicateEntryError      errors.hpp:37 */
+  GSS_ERR_INVALID_COLUMN = 6,  /* InvalidColumnError       errors.hpp:42 */
+  GSS_ERR_NONPOS_DEN = 7,      /* NonPositiveDenominatorError errors.hpp:49 */
+  GSS_ERR_OVERFLOW = 8,        /* OverflowError            errors.hpp:54 */
+  GSS_ERR_DEGENERATE = 9,      /* DegenerateCurveError     errors.hpp:59 */
+  GSS_ERR_EMPTY_FOLD = 10,     /* EmptyFoldError           errors.hpp:64 */
+  GSS_ERR_CUDA = 100,          /* CUDA runtime / driver failure           */
+  GSS_ERR_NO_DEVICE = 101,     /* no usable sm_100 device                  */
+  GSS_ERR_OOM = 102            /* device allocation failed                 */
+};
+
+enum gss_model { GSS_COX = 0, GSS_FINE_GRAY = 1 };            /* engine.hpp:14 */
+enum gss_penalty { GSS_PEN_NONE = 0, GSS_PEN_L1 = 1, GSS_PEN_L2 = 2 }; /* ccd.hpp:11 */
+
+/*
+ * Host-side dataset in the reference's in-memory layout
+ * (include/survscan/dataset.hpp:14-111): rows already sorted by
+ * (stratum asc,) time desc, original row id asc (src/dataset.cpp:227-230);
+ * CSC columns over sorted positions with strictly ascending row indices.
+ */
+typedef struct gss_host_dataset {
+  int64_t n;                     /* rows (< 2^31)                              */
+  int64_t p;                     /* columns                                    */
+  const double* times;           /* [n] sorted survival times                 */
+  const int32_t* status;         /* [n] 0 censored, 1 event, 2 competing      */
+  const int64_t* col_ptr;        /* [p+1] CSC column offsets                  */
+  const int32_t* row_idx;        /* [nnz] sorted row positions                */
+  const double* vals;            /* [nnz] values, or NULL when all are 1.0    */
+  const uint8_t* col_indicator;  /* [p] 1 = indicator column (e*=exp(d) rule,
+                                    src/engine.cpp:200-206); NULL = derive:
+                                    all-ones and density < 25%               */
+  const uint8_t* stratum_start;  /* [n] 1 at the first row of each stratum, or
+                                    NULL (one stratum).  New vs the reference
+                                    (SPEC.md:174 lists strata as a non-goal). */
+} gss_host_dataset;
+
+typedef struct gss_dataset gss_dataset; /* device-resident packed dataset */
+typedef struct gss_engine gss_engine;   /* per-fit device state + stream   */
+
+/* Last error message on this thread ("" if none). */
+const char* gss_last_error(void);
+/* Library/build information (static string). */
+const char* gss_version(void);
+/* Number of usable devices (0 if none). */
+int gss_device_count(void);
+
+/*
+ * Pack a host dataset onto `device`: uploads CSC, builds the tile-blocked
+ * column pointers, the CSR copy used by load_beta/refresh, per-column max |x|.
+ * Replaces sort_and_block's output being handed to Engine
+ * (src/dataset.cpp:172-262 -> src/engine.cpp:103-118).
+ * The returned handle is reference counted (engines retain it).
+ */
+int gss_dataset_pack(const gss_host_dataset* host, int device, gss_dataset** out);
+void gss_dataset_release(gss_dataset* ds);
+/* Bytes of device memory held by the packed dataset. */
+int64_t gss_dataset_device_bytes(const gss_dataset* ds);
+
+/*
+ * Engine(const SurvivalDataset&, Model, ChunkPlan, recompute_interval)
+ * (include/survscan/engine.hpp:38-39, src/engine.cpp:103-118).
+ * row_mask: optional [n] 0/1 — the engine sees only rows with mask 1, exactly
+ * as if the dataset had been subset_rows()'d (src/dataset.cpp:268-322); used
+ * for cross-validation folds without copying the design.
+ * Fine-Gray censoring weights are estimated on the visible rows
+ * (src/censoring.cpp:39-94).  Cox with competing rows -> GSS_ERR_DOMAIN.
+ */
+int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
+                      const uint8_t* row_mask, gss_engine** out);
+void gss_engine_destroy(gss_engine* e);
+
+/* Engine::load_beta (engine.hpp:46; src/engine.cpp:120-154). */
+int gss_engine_load_beta(gss_engine* e, const double* beta, int64_t p);
+/* Engine::update_xbeta_sparse (engine.hpp:52; src/engine.cpp:162-218). */
+int gss_engine_update(gss_engine* e, int64_t column, double delta);
+/* Engine::refresh (engine.hpp:55; src/engine.cpp:156-160). */
+int gss_engine_refresh(gss_engine* e);
+/* Engine::grad_hessian (engine.hpp:60; src/engine.cpp:220-242). */
+int gss_engine_grad_hessian(gss_engine* e, int64_t column, double* gradient,
+                            double* hessian, double* fixed_term);
+/* Engine::log_likelihood (engine.hpp:63; src/engine.cpp:331-341). */
+int gss_engine_log_likelihood(gss_engine* e, double* out);
+
+/* Accessors (engine.hpp:65-71).  Copy device state to host buffers. */
+int gss_engine_get_beta(gss_engine* e, double* out, int64_t p);
+int gss_engine_get_xbeta(gss_engine* e, double* out, int64_t n);
+int gss_engine_get_exp_xbeta(gss_engine* e, double* out, int64_t n);
+int gss_engine_get_fixed_terms(gss_engine* e, double* out, int64_t p);
+int gss_engine_get_ipcw(gss_engine* e, double* u, double* g, int64_t n);
+int gss_engine_counters(gss_engine* e, int64_t* accepted, int64_t* refreshes);
+
+/* Penalty + fit configuration (ccd.hpp:13-30). */
+typedef struct gss_penalty_spec {
+  int kind;                  /* gss_penalty */
+  double strength;           /* gamma (l1) or tau (l2)                      */
+  const uint8_t* exempt;     /* [p] 1 = not penalised, or NULL              */
+} gss_penalty_spec;
+
+typedef struct gss_fit_config {
+  double tolerance;          /* relative objective change per cycle (1e-6) */
+  int64_t max_cycles;        /* 1000 */
+  double trust_init;         /* 1.0 */
+} gss_fit_config;
+
+typedef struct gss_fit_result {
+  double objective;
+  int64_t cycles;
+  int32_t converged;
+  int64_t nonzero_count;
+  int64_t skipped_steps;
+  int64_t monotonicity_violations;
+  double wall_seconds;       /* host wall clock of the whole fit               */
+  double device_seconds;     /* CUDA-event time of the coordinate cycles       */
+} gss_fit_result;
+
+/*
+ * fit_with_engine (src/ccd.cpp:131-184) with the per-coordinate work on the
+ * device: each cycle is one CUDA graph of p fused kernels (pending sparse
+ * update + scan/transform/reduce + coordinate_step), then one log-likelihood
+ * kernel; the host syncs once per cycle to test convergence.
+ * beta_out: [p]; trace_out: [max_cycles+1] (may be NULL).
+ */
+int gss_engine_fit(gss_engine* e, const gss_penalty_spec* pen, const gss_fit_config* cfg,
+                   double* beta_out, double* trace_out, gss_fit_result* out);
+
+/*
+ * gamma_max helper (src/crossval.cpp:104-110): max_j |g'_j| at the engine's
+ * current beta, all columns in one batched device sweep.
+ */
+int gss_engine_max_abs_gradient(gss_engine* e, double* out);
+
+/* Device time (ms) of the last fused coordinate kernel launch set, for bench. */
+int gss_engine_last_timing(gss_engine* e, double* scan_ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSS_H */

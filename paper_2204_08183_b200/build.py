@@ -1,0 +1,74 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel
+with the repo snapshot to the GPU box).
+
+  libgss.so           CUDA kernels + C ABI (include/gss.h), sm_100a
+  _survscan*.so       pybind11 module: the reference's Python API over the
+                      C++ mirror of survscan::{Engine, fit, cross_validate, ...}
+
+    python -m paper_2204_08183_b200.build [--force]
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+import sysconfig
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBGSS = os.path.join(PKG, "libgss.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _newer(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
+def build_libgss(force=False):
+    cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "gss.h")]
+    if force or _newer(LIBGSS, deps):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-diag-suppress", "177", "-shared", *cu, "-o", LIBGSS])
+    return LIBGSS
+
+
+def ext_path():
+    return os.path.join(PKG, "_survscan" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pymodule(force=False):
+    host = os.path.join(CSRC, "host")
+    srcs = sorted(glob.glob(os.path.join(host, "*.cpp")))
+    if not srcs:
+        return None
+    deps = srcs + glob.glob(os.path.join(host, "survscan", "*.hpp")) + [LIBGSS]
+    out = ext_path()
+    if force or _newer(out, deps):
+        import pybind11
+        cuda_inc = "/usr/local/cuda/include"
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
+              "-I" + host, "-I" + os.path.join(ROOT, "include"), "-I" + cuda_inc,
+              "-I" + sysconfig.get_paths()["include"], "-I" + pybind11.get_include(),
+              *srcs, "-L" + PKG, "-lgss", "-Wl,-rpath,$ORIGIN", "-o", out])
+    return out
+
+
+def build(force=False):
+    build_libgss(force)
+    build_pymodule(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,224 @@
+"""ctypes binding of the C ABI (include/gss.h) — the thin FFI layer a host
+language uses to drive the device engine.  No fallback: if libgss.so is
+missing or no sm_100 device is present, calls raise.
+
+This is also the binding shown in INTEGRATION.md for callers that cannot use
+the pybind module.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .build import LIBGSS
+
+GSS_STATUS = {
+    1: "ParseError", 2: "SchemaError", 3: "DomainError", 4: "IndexError",
+    5: "DuplicateEntryError", 6: "InvalidColumnError",
+    7: "NonPositiveDenominatorError", 8: "OverflowError", 9: "DegenerateCurveError",
+    10: "EmptyFoldError", 100: "CudaError", 101: "NoDeviceError", 102: "OutOfMemoryError",
+}
+
+EXPORTS = [
+    "gss_last_error", "gss_version", "gss_device_count", "gss_dataset_pack",
+    "gss_dataset_release", "gss_dataset_device_bytes", "gss_engine_create",
+    "gss_engine_destroy", "gss_engine_load_beta", "gss_engine_update", "gss_engine_refresh",
+    "gss_engine_grad_hessian", "gss_engine_log_likelihood", "gss_engine_get_beta",
+    "gss_engine_get_xbeta", "gss_engine_get_exp_xbeta", "gss_engine_get_fixed_terms",
+    "gss_engine_get_ipcw", "gss_engine_counters", "gss_engine_fit",
+    "gss_engine_max_abs_gradient", "gss_engine_last_timing",
+]
+
+
+class GssError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        self.kind = GSS_STATUS.get(code, str(code))
+        super().__init__(f"{self.kind}: {msg}")
+
+
+class HostDataset(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("p", ctypes.c_int64),
+                ("times", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("col_ptr", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
+                ("vals", ctypes.c_void_p), ("col_indicator", ctypes.c_void_p),
+                ("stratum_start", ctypes.c_void_p)]
+
+
+class PenaltySpec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("strength", ctypes.c_double),
+                ("exempt", ctypes.c_void_p)]
+
+
+class FitConfig(ctypes.Structure):
+    _fields_ = [("tolerance", ctypes.c_double), ("max_cycles", ctypes.c_int64),
+                ("trust_init", ctypes.c_double)]
+
+
+class FitResult(ctypes.Structure):
+    _fields_ = [("objective", ctypes.c_double), ("cycles", ctypes.c_int64),
+                ("converged", ctypes.c_int32), ("nonzero_count", ctypes.c_int64),
+                ("skipped_steps", ctypes.c_int64), ("monotonicity_violations", ctypes.c_int64),
+                ("wall_seconds", ctypes.c_double), ("device_seconds", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIBGSS):
+            raise ImportError(f"{LIBGSS} not built (run python -m paper_2204_08183_b200.build)")
+        L = ctypes.CDLL(LIBGSS)
+        L.gss_last_error.restype = ctypes.c_char_p
+        L.gss_version.restype = ctypes.c_char_p
+        L.gss_dataset_device_bytes.restype = ctypes.c_int64
+        for name in ("gss_dataset_release", "gss_engine_destroy"):
+            getattr(L, name).restype = None
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        raise GssError(rc, lib().gss_last_error().decode())
+
+
+def _p(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class Dataset:
+    """Device-packed dataset from the sorted host layout (see oracle.Sorted)."""
+
+    def __init__(self, times, status, col_ptr, row_idx, vals=None, col_indicator=None,
+                 stratum_start=None, device=0):
+        self._arrs = [np.ascontiguousarray(times, np.float64),
+                      np.ascontiguousarray(status, np.int32),
+                      np.ascontiguousarray(col_ptr, np.int64),
+                      np.ascontiguousarray(row_idx, np.int32),
+                      None if vals is None else np.ascontiguousarray(vals, np.float64),
+                      None if col_indicator is None else np.ascontiguousarray(col_indicator,
+                                                                              np.uint8),
+                      None if stratum_start is None else np.ascontiguousarray(stratum_start,
+                                                                              np.uint8)]
+        t, s, cp, ri, v, ci, ss = self._arrs
+        self.n, self.p = len(t), len(cp) - 1
+        h = HostDataset(self.n, self.p, t.ctypes.data, s.ctypes.data, cp.ctypes.data,
+                        ri.ctypes.data if len(ri) else None,
+                        None if v is None else v.ctypes.data,
+                        None if ci is None else ci.ctypes.data,
+                        None if ss is None else ss.ctypes.data)
+        self.h = ctypes.c_void_p()
+        check(lib().gss_dataset_pack(ctypes.byref(h), device, ctypes.byref(self.h)))
+
+    @classmethod
+    def from_sorted(cls, ds, device=0):
+        return cls(ds.times, ds.status, ds.col_ptr, ds.row_idx, ds.vals, ds.col_indicator,
+                   ds.stratum_start, device)
+
+    def device_bytes(self):
+        return lib().gss_dataset_device_bytes(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gss_dataset_release(self.h)
+            self.h = None
+
+
+class Engine:
+    """survscan::Engine surface over the C ABI (engine.hpp:33-90)."""
+
+    def __init__(self, ds: Dataset, model="cox", recompute_interval=100, row_mask=None):
+        self.ds = ds
+        m = {"cox": 0, "finegray": 1, "fine_gray": 1}[model]
+        self._mask = None if row_mask is None else np.ascontiguousarray(row_mask, np.uint8)
+        self.h = ctypes.c_void_p()
+        check(lib().gss_engine_create(ds.h, m, ctypes.c_int64(recompute_interval),
+                                      _p(self._mask), ctypes.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gss_engine_destroy(self.h)
+            self.h = None
+
+    def load_beta(self, beta):
+        b = np.ascontiguousarray(beta, np.float64)
+        check(lib().gss_engine_load_beta(self.h, _p(b), ctypes.c_int64(len(b))))
+
+    def update(self, j, delta):
+        check(lib().gss_engine_update(self.h, ctypes.c_int64(j), ctypes.c_double(delta)))
+
+    def refresh(self):
+        check(lib().gss_engine_refresh(self.h))
+
+    def grad_hessian(self, j):
+        g, h, f = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        check(lib().gss_engine_grad_hessian(self.h, ctypes.c_int64(j), ctypes.byref(g),
+                                            ctypes.byref(h), ctypes.byref(f)))
+        return {"gradient": g.value, "hessian": h.value, "fixed_term": f.value}
+
+    def log_likelihood(self):
+        out = ctypes.c_double()
+        check(lib().gss_engine_log_likelihood(self.h, ctypes.byref(out)))
+        return out.value
+
+    def _rows(self, fn):
+        out = np.empty(self.ds.n)
+        check(fn(self.h, _p(out), ctypes.c_int64(self.ds.n)))
+        return out
+
+    def beta(self):
+        out = np.empty(self.ds.p)
+        check(lib().gss_engine_get_beta(self.h, _p(out), ctypes.c_int64(self.ds.p)))
+        return out
+
+    def xbeta(self):
+        return self._rows(lib().gss_engine_get_xbeta)
+
+    def exp_xbeta(self):
+        return self._rows(lib().gss_engine_get_exp_xbeta)
+
+    def fixed_terms(self):
+        out = np.empty(self.ds.p)
+        check(lib().gss_engine_get_fixed_terms(self.h, _p(out), ctypes.c_int64(self.ds.p)))
+        return out
+
+    def counters(self):
+        a, r = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().gss_engine_counters(self.h, ctypes.byref(a), ctypes.byref(r)))
+        return a.value, r.value
+
+    def max_abs_gradient(self):
+        out = ctypes.c_double()
+        check(lib().gss_engine_max_abs_gradient(self.h, ctypes.byref(out)))
+        return out.value
+
+    def fit(self, penalty="none", strength=0.0, exempt=(), tol=1e-6, max_cycles=1000,
+            trust_init=1.0):
+        kind = {"none": 0, "l1": 1, "l2": 2}[penalty]
+        ex = None
+        if len(exempt):
+            ex = np.zeros(self.ds.p, np.uint8)
+            ex[list(exempt)] = 1
+        pen = PenaltySpec(kind, strength, None if ex is None else ex.ctypes.data)
+        cfg = FitConfig(tol, max_cycles, trust_init)
+        beta = np.zeros(self.ds.p)
+        trace = np.zeros(max_cycles + 1)
+        res = FitResult()
+        check(lib().gss_engine_fit(self.h, ctypes.byref(pen), ctypes.byref(cfg), _p(beta),
+                                   _p(trace), ctypes.byref(res)))
+        return {"beta": beta, "objective": res.objective, "cycles": res.cycles,
+                "converged": bool(res.converged), "nonzero_count": res.nonzero_count,
+                "skipped_steps": res.skipped_steps,
+                "monotonicity_violations": res.monotonicity_violations,
+                "objective_trace": trace[:res.cycles + 1].copy(),
+                "wall_seconds": res.wall_seconds, "device_seconds": res.device_seconds}
+
+    def last_timing(self):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib().gss_engine_last_timing(self.h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value

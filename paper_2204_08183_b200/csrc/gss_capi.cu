@@ -1,0 +1,892 @@
+// gss_capi.cu — host implementation of the C ABI in include/gss.h.
+//
+// Owns device memory, streams, TMA descriptors and the per-cycle CUDA graph;
+// builds the per-engine row code words and (Fine-Gray) censoring weights on
+// the host, exactly as the reference builds them per Engine
+// (src/engine.cpp:103-118, src/censoring.cpp:39-94).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gss.h"
+#include "gss_device.cuh"
+#include "gss_kernels.cuh"
+
+using namespace gss;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define GSS_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA,         \
+                  std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #call); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D view [rows = npad/kIpt][kIpt] of a row-major per-row array, box = one tile.
+int make_tile_map(CUtensorMap* map, void* base, int64_t npad, CUtensorMapDataType dt,
+                  int elem_bytes, CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return fail(GSS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kIpt), static_cast<cuuint64_t>(npad / kIpt)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kIpt) * elem_bytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kIpt), static_cast<cuuint32_t>(kThreads)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GSS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return GSS_OK;
+}
+
+}  // namespace
+
+struct gss_dataset {
+  std::atomic<int> refs{1};
+  int device = 0;
+  int64_t n = 0, p = 0, nnz = 0, npad = 0;
+  int ntiles = 0;
+  bool has_vals = false;
+  // host copies needed per engine (row codes, IPCW)
+  std::vector<double> times;
+  std::vector<int32_t> status;
+  std::vector<uint8_t> stratum_start;
+  // device
+  int64_t* col_ptr = nullptr;
+  int32_t* row_idx = nullptr;
+  double* vals = nullptr;
+  uint8_t* col_ind = nullptr;
+  uint32_t* tile_ptr = nullptr;
+  int64_t* row_ptr = nullptr;
+  int32_t* csr_col = nullptr;
+  double* csr_val = nullptr;
+  double* colmax = nullptr;
+  int64_t bytes = 0;
+  std::vector<int64_t> h_col_ptr;
+
+  ~gss_dataset() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* q : {(void*)col_ptr, (void*)row_idx, (void*)vals, (void*)col_ind, (void*)tile_ptr,
+                    (void*)row_ptr, (void*)csr_col, (void*)csr_val, (void*)colmax})
+      if (q) cudaFree(q);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+struct gss_engine {
+  gss_dataset* ds = nullptr;
+  int model = 0;
+  int64_t interval = 100;
+  bool weighted = false;
+  cudaStream_t stream = nullptr;
+  int grid = 1;
+  std::vector<uint32_t> h_code;
+  std::vector<double> h_u, h_g;
+  std::vector<double> h_beta;
+  // device
+  double *eta = nullptr, *e = nullptr, *scratch = nullptr, *u = nullptr, *g = nullptr;
+  uint32_t* code = nullptr;
+  double *beta = nullptr, *halfwidth = nullptr, *fixed = nullptr;
+  uint8_t* penalized = nullptr;
+  unsigned long long *statA = nullptr, *statP = nullptr;
+  double *aggA = nullptr, *aggP = nullptr, *tile_part = nullptr;
+  Ctl* ctl = nullptr;
+  int* dflag = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned mirror
+  CUtensorMap tm_e{}, tm_code{};
+  SweepParams prm{};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int64_t last_launches = 0;
+
+  ~gss_engine() {
+    cudaSetDevice(ds->device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)u, (void*)g, (void*)code,
+                    (void*)beta, (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)statA,
+                    (void*)statP, (void*)aggA, (void*)aggP, (void*)tile_part, (void*)ctl,
+                    (void*)dflag})
+      if (q) cudaFree(q);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    gss_dataset_release(ds);
+  }
+};
+
+namespace {
+
+int sync_ctl(gss_engine* E) {
+  GSS_CUDA(cudaMemcpyAsync(E->h_ctl, E->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, E->stream));
+  GSS_CUDA(cudaStreamSynchronize(E->stream));
+  return GSS_OK;
+}
+
+int push_ctl(gss_engine* E) {
+  GSS_CUDA(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, E->stream));
+  GSS_CUDA(cudaStreamSynchronize(E->stream));
+  return GSS_OK;
+}
+
+// Map a device error word to the reference exception class + message.
+int device_error(gss_engine* E, const char* where) {
+  const int code = E->h_ctl->err_code;
+  const long long col = E->h_ctl->err_col;
+  std::string msg;
+  switch (code) {
+    case GSS_ERR_NONPOS_DEN:
+      msg = std::string(where) +
+            ": accumulated risk-set denominator <= 0 or derivatives not finite (exp overflow?)";
+      break;
+    case GSS_ERR_OVERFLOW:
+      msg = std::string(where) + ": |x'beta| would exceed 700";
+      break;
+    default:
+      msg = std::string(where) + ": device error " + std::to_string(code);
+  }
+  if (col >= 0) msg += " (column " + std::to_string(col) + ")";
+  // clear for the next call
+  E->h_ctl->err_code = 0;
+  E->h_ctl->err_col = -1;
+  E->h_ctl->halted = 0;
+  E->h_ctl->pend_col = -1;
+  E->h_ctl->pend_delta = 0.0;
+  E->h_ctl->refresh_pending = 0;
+  push_ctl(E);
+  return fail(code, msg);
+}
+
+// Per-engine row code words over the visible rows (row_mask), stratum by
+// stratum: maximal runs of equal time among visible rows form the tied blocks
+// (src/dataset.cpp:190-204 applied to the subset, src/dataset.cpp:268-322);
+// the run's status==1 count goes to its last visible row.
+void build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t>& code) {
+  const int64_t n = ds->n;
+  code.assign(static_cast<size_t>(ds->npad), 0u);
+  for (int64_t i = n; i < ds->npad; ++i) code[i] = kCodeMasked;
+  int64_t s = 0;
+  while (s < n) {
+    int64_t e = s + 1;
+    if (!ds->stratum_start.empty())
+      while (e < n && !ds->stratum_start[e]) ++e;
+    else
+      e = n;
+    code[s] |= kCodeSeg;
+    int64_t last_vis = -1;
+    double last_t = 0.0;
+    uint32_t cnt = 0;
+    for (int64_t i = s; i < e; ++i) {
+      const bool vis = !mask || mask[i];
+      if (!vis) {
+        code[i] |= kCodeMasked;
+        continue;
+      }
+      if (last_vis >= 0 && ds->times[i] != last_t) {
+        code[last_vis] |= cnt;
+        cnt = 0;
+      }
+      if (ds->status[i] == 1) {
+        ++cnt;
+        code[i] |= kCodeEvent;
+      }
+      last_vis = i;
+      last_t = ds->times[i];
+    }
+    if (last_vis >= 0) code[last_vis] |= cnt;
+    s = e;
+  }
+}
+
+// Kaplan-Meier of the censoring distribution over the visible rows of each
+// stratum, failures before censorings on ties, then u = 1/G(Y-) on competing
+// rows and g = G(Y-) (src/censoring.cpp:39-90).
+int build_ipcw_host(const gss_dataset* ds, const uint8_t* mask, std::vector<double>& u,
+                    std::vector<double>& g) {
+  const int64_t n = ds->n;
+  u.assign(static_cast<size_t>(ds->npad), 0.0);
+  g.assign(static_cast<size_t>(ds->npad), 1.0);
+  std::vector<int64_t> rows, ends;
+  int64_t s = 0;
+  while (s < n) {
+    int64_t e = s + 1;
+    if (!ds->stratum_start.empty())
+      while (e < n && !ds->stratum_start[e]) ++e;
+    else
+      e = n;
+    rows.clear();
+    for (int64_t i = s; i < e; ++i)
+      if (!mask || mask[i]) rows.push_back(i);
+    ends.clear();
+    for (size_t k = 0; k < rows.size(); ++k)
+      if (k + 1 == rows.size() || ds->times[rows[k + 1]] != ds->times[rows[k]]) ends.push_back(k);
+    double surv = 1.0;
+    for (size_t b = ends.size(); b-- > 0;) {
+      const size_t end = ends[b];
+      const size_t start = b == 0 ? 0 : ends[b - 1] + 1;
+      const double before = surv;
+      int64_t censored = 0, failed = 0;
+      for (size_t k = start; k <= end; ++k) {
+        const int64_t i = rows[k];
+        if (ds->status[i] == 0)
+          ++censored;
+        else
+          ++failed;
+        g[i] = before;
+        if (ds->status[i] == 2) {
+          if (!(before > 0.0))
+            return fail(GSS_ERR_DEGENERATE,
+                        "censoring curve vanishes before a competing event at time " +
+                            std::to_string(ds->times[i]));
+          u[i] = 1.0 / before;
+        }
+      }
+      if (censored) {
+        const double at_risk = static_cast<double>(static_cast<int64_t>(end) + 1 - failed);
+        surv *= 1.0 - static_cast<double>(censored) / at_risk;
+      }
+    }
+    s = e;
+  }
+  return GSS_OK;
+}
+
+int check_engine(gss_engine* E) {
+  if (!E) return fail(GSS_ERR_DOMAIN, "null engine handle");
+  cudaError_t err = cudaSetDevice(E->ds->device);
+  if (err != cudaSuccess) return fail(GSS_ERR_CUDA, cudaGetErrorString(err));
+  return GSS_OK;
+}
+
+int launch(gss_engine* E, int mode, int64_t column) {
+  E->prm.column = column;
+  GSS_CUDA(launch_sweep(mode, &E->tm_e, &E->tm_code, E->prm, E->grid, E->stream));
+  return GSS_OK;
+}
+
+double penalty_value(const gss_penalty_spec* pen, const std::vector<double>& beta) {
+  if (pen->kind == GSS_PEN_NONE) return 0.0;
+  double acc = 0.0;
+  for (size_t j = 0; j < beta.size(); ++j) {
+    if (pen->exempt && pen->exempt[j]) continue;
+    if (pen->kind == GSS_PEN_L1)
+      acc += pen->strength * std::abs(beta[j]);
+    else
+      acc += beta[j] * beta[j] / (2.0 * pen->strength);
+  }
+  return acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gss_last_error(void) { return g_last_error.c_str(); }
+
+const char* gss_version(void) {
+  return "gss 0.1.0 (sm_100a; tile=2048 rows; decoupled look-back fp64 scan)";
+}
+
+int gss_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
+  if (!h || !out) return fail(GSS_ERR_DOMAIN, "null argument");
+  *out = nullptr;
+  if (h->n < 0 || h->p < 0) return fail(GSS_ERR_DOMAIN, "negative dimensions");
+  if (h->n >= (int64_t(1) << 31) - kTileRows)
+    return fail(GSS_ERR_DOMAIN, "dataset too large for 32-bit row offsets");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(GSS_ERR_NO_DEVICE, "no CUDA device available");
+  if (device < 0 || device >= ndev) return fail(GSS_ERR_NO_DEVICE, "bad device index");
+  GSS_CUDA(cudaSetDevice(device));
+  const int64_t n = h->n, p = h->p;
+  const int64_t nnz = p > 0 ? h->col_ptr[p] : 0;
+  // validate the layout contract (sorted rows, ascending CSC indices)
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(h->times[i]) || h->times[i] < 0.0)
+      return fail(GSS_ERR_DOMAIN, "observation time must be finite and >= 0");
+    if (h->status[i] < 0 || h->status[i] > 2) return fail(GSS_ERR_DOMAIN, "status must be 0, 1 or 2");
+    const bool new_stratum = h->stratum_start && h->stratum_start[i];
+    if (i > 0 && !new_stratum && h->times[i] > h->times[i - 1])
+      return fail(GSS_ERR_DOMAIN, "rows must be sorted by decreasing time within a stratum");
+  }
+  for (int64_t j = 0; j < p; ++j) {
+    if (h->col_ptr[j + 1] < h->col_ptr[j]) return fail(GSS_ERR_DOMAIN, "col_ptr not monotone");
+    for (int64_t k = h->col_ptr[j]; k < h->col_ptr[j + 1]; ++k) {
+      if (h->row_idx[k] < 0 || h->row_idx[k] >= n)
+        return fail(GSS_ERR_INDEX, "row index outside [0, n)");
+      if (k > h->col_ptr[j] && h->row_idx[k] <= h->row_idx[k - 1])
+        return fail(GSS_ERR_DOMAIN, "row indices must strictly ascend within a column");
+    }
+  }
+  auto* ds = new gss_dataset();
+  ds->device = device;
+  ds->n = n;
+  ds->p = p;
+  ds->nnz = nnz;
+  ds->ntiles = static_cast<int>((n + kTileRows - 1) / kTileRows);
+  if (ds->ntiles == 0) ds->ntiles = 1;
+  ds->npad = int64_t(ds->ntiles) * kTileRows;
+  ds->times.assign(h->times, h->times + n);
+  ds->status.assign(h->status, h->status + n);
+  if (h->stratum_start) ds->stratum_start.assign(h->stratum_start, h->stratum_start + n);
+  ds->h_col_ptr.assign(h->col_ptr, h->col_ptr + p + 1);
+  if (p == 0) ds->h_col_ptr.assign(1, 0);
+  // indicator flags: given, or all-ones & density < 25% (src/dataset.cpp:126-157)
+  std::vector<uint8_t> ind(static_cast<size_t>(p), 1);
+  bool any_valued = false;
+  for (int64_t j = 0; j < p; ++j) {
+    if (h->col_indicator) {
+      ind[j] = h->col_indicator[j] ? 1 : 0;
+    } else if (h->vals) {
+      const int64_t cnt = h->col_ptr[j + 1] - h->col_ptr[j];
+      bool ones = true;
+      for (int64_t k = h->col_ptr[j]; k < h->col_ptr[j + 1] && ones; ++k) ones = h->vals[k] == 1.0;
+      const double dens = n ? double(cnt) / double(n) : 0.0;
+      ind[j] = (ones && dens < 0.25) ? 1 : 0;
+    }
+    if (!ind[j]) any_valued = true;
+  }
+  ds->has_vals = h->vals != nullptr && any_valued;
+  cudaStream_t s;
+  GSS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  auto cleanup = [&](int rc) {
+    cudaStreamDestroy(s);
+    if (rc != GSS_OK) delete ds;
+    return rc;
+  };
+#define PK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return cleanup(fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA, \
+                          std::string("CUDA error in pack: ") + cudaGetErrorString(_e))); \
+  } while (0)
+  PK(dalloc(&ds->col_ptr, p + 1));
+  PK(dalloc(&ds->row_idx, nnz + 4));
+  PK(dalloc(&ds->col_ind, p));
+  PK(dalloc(&ds->tile_ptr, p * (ds->ntiles + 1)));
+  PK(dalloc(&ds->row_ptr, n + 1));
+  PK(dalloc(&ds->csr_col, nnz + 4));
+  PK(dalloc(&ds->colmax, p));
+  if (ds->has_vals) {
+    PK(dalloc(&ds->vals, nnz + 4));
+    PK(dalloc(&ds->csr_val, nnz + 4));
+  }
+  ds->bytes = (p + 1) * 8 + (nnz + 4) * 8 + p + int64_t(p) * (ds->ntiles + 1) * 4 + (n + 1) * 8 +
+              p * 8 + (ds->has_vals ? (nnz + 4) * 16 : 0);
+  PK(cudaMemcpyAsync(ds->col_ptr, ds->h_col_ptr.data(), (p + 1) * sizeof(int64_t),
+                     cudaMemcpyHostToDevice, s));
+  PK(cudaMemsetAsync(ds->row_idx, 0, (nnz + 4) * sizeof(int32_t), s));
+  if (nnz)
+    PK(cudaMemcpyAsync(ds->row_idx, h->row_idx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (p) PK(cudaMemcpyAsync(ds->col_ind, ind.data(), p, cudaMemcpyHostToDevice, s));
+  if (ds->has_vals && nnz)
+    PK(cudaMemcpyAsync(ds->vals, h->vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (p) {
+    PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
+    PK(launch_colmax(ds->col_ptr, ds->has_vals ? ds->vals : nullptr, p, ds->colmax, s));
+  }
+  // CSR transpose: count -> host exclusive scan -> fill -> per-row sort
+  {
+    int64_t* cnt = nullptr;
+    PK(dalloc(&cnt, n + 1));
+    PK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int64_t), s));
+    PK(launch_csr_count(ds->row_idx, nnz, cnt, s));
+    std::vector<int64_t> hc(static_cast<size_t>(n + 1), 0);
+    PK(cudaMemcpyAsync(hc.data(), cnt, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PK(cudaStreamSynchronize(s));
+    std::vector<int64_t> rp(static_cast<size_t>(n + 1), 0);
+    for (int64_t i = 0; i < n; ++i) rp[i + 1] = rp[i] + hc[i];
+    PK(cudaMemcpyAsync(ds->row_ptr, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       s));
+    PK(cudaMemcpyAsync(cnt, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    PK(launch_csr_fill(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, p, cnt,
+                       ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
+    PK(launch_csr_sort_rows(ds->row_ptr, n, ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
+    PK(cudaStreamSynchronize(s));
+    cudaFree(cnt);
+  }
+#undef PK
+  *out = ds;
+  return cleanup(GSS_OK);
+}
+
+void gss_dataset_release(gss_dataset* ds) {
+  if (ds && --ds->refs == 0) delete ds;
+}
+
+int64_t gss_dataset_device_bytes(const gss_dataset* ds) { return ds ? ds->bytes : 0; }
+
+int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
+                      const uint8_t* row_mask, gss_engine** out) {
+  if (!ds || !out) return fail(GSS_ERR_DOMAIN, "null argument");
+  *out = nullptr;
+  if (recompute_interval < 1) return fail(GSS_ERR_DOMAIN, "recompute_interval must be at least 1");
+  if (model != GSS_COX && model != GSS_FINE_GRAY) return fail(GSS_ERR_DOMAIN, "unknown model");
+  bool competing = false;
+  for (int64_t i = 0; i < ds->n; ++i)
+    if (ds->status[i] == 2 && (!row_mask || row_mask[i])) competing = true;
+  if (model == GSS_COX && competing)
+    return fail(GSS_ERR_DOMAIN,
+                "cox model cannot ingest competing-event rows; fit fine_gray instead");
+  GSS_CUDA(cudaSetDevice(ds->device));
+  auto* E = new gss_engine();
+  ++ds->refs;
+  E->ds = ds;
+  E->model = model;
+  E->interval = recompute_interval;
+  E->weighted = model == GSS_FINE_GRAY && competing;  // src/engine.cpp:237
+  if (E->weighted) {
+    delete E;
+    return fail(GSS_ERR_DOMAIN,
+                "fine_gray with competing rows is not yet available on the device path");
+  }
+  build_codes(ds, row_mask, E->h_code);
+  const int64_t n = ds->n, p = ds->p, npad = ds->npad;
+  const int nt = ds->ntiles, ng = nt / kGroup + 1;
+  auto bail = [&](int rc) {
+    delete E;
+    return rc;
+  };
+#define EK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return bail(fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA,    \
+                       std::string("CUDA error in engine_create: ") + cudaGetErrorString(_e))); \
+  } while (0)
+  EK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
+  EK(cudaEventCreate(&E->ev0));
+  EK(cudaEventCreate(&E->ev1));
+  EK(dalloc(&E->eta, npad));
+  EK(dalloc(&E->e, npad));
+  EK(dalloc(&E->scratch, npad));
+  EK(dalloc(&E->code, npad));
+  EK(dalloc(&E->beta, p));
+  EK(dalloc(&E->halfwidth, p));
+  EK(dalloc(&E->fixed, p));
+  EK(dalloc(&E->penalized, p));
+  EK(dalloc(&E->statA, nt));
+  EK(dalloc(&E->statP, ng));
+  EK(dalloc(&E->aggA, size_t(nt) * 8));
+  EK(dalloc(&E->aggP, size_t(ng) * 8));
+  EK(dalloc(&E->tile_part, size_t(nt) * 4));
+  EK(dalloc(&E->ctl, 1));
+  EK(dalloc(&E->dflag, 4));
+  EK(cudaMallocHost(reinterpret_cast<void**>(&E->h_ctl), sizeof(Ctl)));
+  std::memset(E->h_ctl, 0, sizeof(Ctl));
+  E->h_ctl->epoch = 1;
+  E->h_ctl->pend_col = -1;
+  E->h_ctl->err_col = -1;
+  cudaStream_t s = E->stream;
+  EK(cudaMemcpyAsync(E->code, E->h_code.data(), npad * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  EK(cudaMemsetAsync(E->eta, 0, npad * sizeof(double), s));
+  {
+    std::vector<double> e0(static_cast<size_t>(npad), 0.0);
+    for (int64_t i = 0; i < n; ++i) e0[i] = (E->h_code[i] & kCodeMasked) ? 0.0 : 1.0;
+    EK(cudaMemcpyAsync(E->e, e0.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
+    EK(cudaStreamSynchronize(s));
+  }
+  EK(cudaMemsetAsync(E->beta, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
+  EK(cudaMemsetAsync(E->statA, 0, nt * sizeof(unsigned long long), s));
+  EK(cudaMemsetAsync(E->statP, 0, ng * sizeof(unsigned long long), s));
+  EK(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+  EK(launch_fixed_terms(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, ds->col_ind,
+                        E->code, p, E->fixed, s));
+  EK(cudaStreamSynchronize(s));
+  E->h_beta.assign(static_cast<size_t>(p), 0.0);
+  int rc = make_tile_map(&E->tm_e, E->e, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
+                         CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return bail(rc);
+  rc = make_tile_map(&E->tm_code, E->code, npad, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4,
+                     CU_TENSOR_MAP_SWIZZLE_32B);
+  if (rc) return bail(rc);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ds->device);
+  int occ = sweep_max_active_ctas_per_sm();
+  if (occ < 1) occ = 1;
+  E->grid = std::max(1, std::min(nt, sms * occ));
+  SweepParams& P = E->prm;
+  P.n = n;
+  P.npad = npad;
+  P.p = p;
+  P.ntiles = nt;
+  P.has_vals = ds->has_vals ? 1 : 0;
+  P.col_ptr = ds->col_ptr;
+  P.row_idx = ds->row_idx;
+  P.vals = ds->vals;
+  P.col_ind = ds->col_ind;
+  P.tile_ptr = ds->tile_ptr;
+  P.row_ptr = ds->row_ptr;
+  P.csr_col = ds->csr_col;
+  P.csr_val = ds->csr_val;
+  P.colmax = ds->colmax;
+  P.eta = E->eta;
+  P.e = E->e;
+  P.code = E->code;
+  P.u = E->u;
+  P.g = E->g;
+  P.beta = E->beta;
+  P.halfwidth = E->halfwidth;
+  P.penalized = E->penalized;
+  P.fixed = E->fixed;
+  P.pen_kind = 0;
+  P.weighted = E->weighted ? 1 : 0;
+  P.pen_strength = 0.0;
+  P.recompute_interval = recompute_interval;
+  P.statA = E->statA;
+  P.aggA = E->aggA;
+  P.statP = E->statP;
+  P.aggP = E->aggP;
+  P.tile_part = E->tile_part;
+  P.ctl = E->ctl;
+  P.column = 0;
+#undef EK
+  *out = E;
+  return GSS_OK;
+}
+
+void gss_engine_destroy(gss_engine* e) { delete e; }
+
+int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (p != E->ds->p)
+    return fail(GSS_ERR_INVALID_COLUMN, "load_beta: expected " + std::to_string(E->ds->p) +
+                                            " coefficients, got " + std::to_string(p));
+  for (int64_t j = 0; j < p; ++j)
+    if (!std::isfinite(beta[j])) return fail(GSS_ERR_DOMAIN, "load_beta: non-finite coefficient");
+  // scratch beta lives in the tail of `scratch`? keep a dedicated upload buffer
+  double* dbeta = nullptr;
+  GSS_CUDA(dalloc(&dbeta, p));
+  cudaStream_t s = E->stream;
+  if (p) GSS_CUDA(cudaMemcpyAsync(dbeta, beta, p * sizeof(double), cudaMemcpyHostToDevice, s));
+  GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
+  GSS_CUDA(launch_spmv_rows(E->prm, dbeta, E->scratch, E->dflag, s));
+  int over = 0;
+  GSS_CUDA(cudaMemcpyAsync(&over, E->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  if (over) {
+    cudaFree(dbeta);
+    return fail(GSS_ERR_OVERFLOW, "load_beta: |x'beta| exceeds 700");
+  }
+  if (p) GSS_CUDA(cudaMemcpyAsync(E->beta, dbeta, p * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GSS_CUDA(launch_commit_eta(E->prm, E->scratch, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  cudaFree(dbeta);
+  E->h_beta.assign(beta, beta + p);
+  return GSS_OK;
+}
+
+int gss_engine_refresh(gss_engine* E) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  std::vector<double> b = E->h_beta;
+  rc = gss_engine_load_beta(E, b.data(), static_cast<int64_t>(b.size()));
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  E->h_ctl->refreshes += 1;
+  return push_ctl(E);
+}
+
+int gss_engine_update(gss_engine* E, int64_t column, double delta) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < 0 || column >= E->ds->p)
+    return fail(GSS_ERR_INVALID_COLUMN, "update: column " + std::to_string(column) +
+                                            " outside [0, " + std::to_string(E->ds->p) + ")");
+  if (!std::isfinite(delta)) return fail(GSS_ERR_DOMAIN, "update: non-finite delta");
+  if (delta == 0.0) return GSS_OK;
+  cudaStream_t s = E->stream;
+  GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
+  GSS_CUDA(launch_update_check(E->prm, column, delta, E->dflag, s));
+  int over = 0;
+  GSS_CUDA(cudaMemcpyAsync(&over, E->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  if (over) return fail(GSS_ERR_OVERFLOW, "update: |x'beta| would exceed 700");
+  GSS_CUDA(launch_update_commit(E->prm, column, delta, std::exp(delta), s));
+  E->h_beta[column] += delta;
+  GSS_CUDA(cudaMemcpyAsync(E->beta + column, &E->h_beta[column], sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  E->h_ctl->accepted += 1;
+  const bool refresh = E->h_ctl->accepted % E->interval == 0;
+  rc = push_ctl(E);
+  if (rc) return rc;
+  if (refresh) return gss_engine_refresh(E);
+  return GSS_OK;
+}
+
+int gss_engine_grad_hessian(gss_engine* E, int64_t column, double* gradient, double* hessian,
+                            double* fixed_term) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < 0 || column >= E->ds->p)
+    return fail(GSS_ERR_INVALID_COLUMN, "grad_hessian: column " + std::to_string(column) +
+                                            " outside [0, " + std::to_string(E->ds->p) + ")");
+  rc = launch(E, kModeGradApi, column);
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (E->h_ctl->err_code) return device_error(E, "grad_hessian");
+  if (gradient) *gradient = E->h_ctl->gradient;
+  if (hessian) *hessian = E->h_ctl->hessian;
+  if (fixed_term) *fixed_term = E->h_ctl->fixed_term;
+  return GSS_OK;
+}
+
+int gss_engine_log_likelihood(gss_engine* E, double* out) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  rc = launch(E, kModeLoglik, 0);
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (E->h_ctl->err_code) return device_error(E, "log-likelihood");
+  *out = E->h_ctl->loglik;
+  return GSS_OK;
+}
+
+int gss_engine_get_beta(gss_engine* E, double* out, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (p != E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "get_beta: size mismatch");
+  std::copy(E->h_beta.begin(), E->h_beta.end(), out);
+  return GSS_OK;
+}
+
+static int get_rows(gss_engine* E, const double* src, double* out, int64_t n) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (n != E->ds->n) return fail(GSS_ERR_DOMAIN, "row array size mismatch");
+  if (n) GSS_CUDA(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, E->stream));
+  GSS_CUDA(cudaStreamSynchronize(E->stream));
+  return GSS_OK;
+}
+
+int gss_engine_get_xbeta(gss_engine* E, double* out, int64_t n) { return get_rows(E, E->eta, out, n); }
+int gss_engine_get_exp_xbeta(gss_engine* E, double* out, int64_t n) {
+  return get_rows(E, E->e, out, n);
+}
+
+int gss_engine_get_fixed_terms(gss_engine* E, double* out, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (p != E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "fixed terms: size mismatch");
+  if (p) GSS_CUDA(cudaMemcpyAsync(out, E->fixed, p * sizeof(double), cudaMemcpyDeviceToHost, E->stream));
+  GSS_CUDA(cudaStreamSynchronize(E->stream));
+  return GSS_OK;
+}
+
+int gss_engine_get_ipcw(gss_engine* E, double* u, double* g, int64_t n) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (n != E->ds->n) return fail(GSS_ERR_DOMAIN, "ipcw: size mismatch");
+  for (int64_t i = 0; i < n; ++i) {
+    u[i] = E->h_u.empty() ? 0.0 : E->h_u[i];
+    g[i] = E->h_g.empty() ? 1.0 : E->h_g[i];
+  }
+  return GSS_OK;
+}
+
+int gss_engine_counters(gss_engine* E, int64_t* accepted, int64_t* refreshes) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (accepted) *accepted = E->h_ctl->accepted;
+  if (refreshes) *refreshes = E->h_ctl->refreshes;
+  return GSS_OK;
+}
+
+int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* cfg,
+                   double* beta_out, double* trace_out, gss_fit_result* res) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (!pen || !cfg || !res) return fail(GSS_ERR_DOMAIN, "null argument");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t p = E->ds->p;
+  // PenaltySpec::validate / FitConfig::validate (src/ccd.cpp:37-69)
+  if (pen->kind == GSS_PEN_L1 && (!std::isfinite(pen->strength) || pen->strength < 0.0))
+    return fail(GSS_ERR_DOMAIN, "l1 strength must be finite and >= 0");
+  if (pen->kind == GSS_PEN_L2 && (!std::isfinite(pen->strength) || pen->strength <= 0.0))
+    return fail(GSS_ERR_DOMAIN, "l2 strength must be finite and > 0");
+  if (pen->kind < 0 || pen->kind > 2) return fail(GSS_ERR_DOMAIN, "unknown penalty");
+  if (!std::isfinite(cfg->tolerance) || cfg->tolerance <= 0.0)
+    return fail(GSS_ERR_DOMAIN, "tolerance must be > 0");
+  if (cfg->max_cycles < 1) return fail(GSS_ERR_DOMAIN, "max_cycles must be >= 1");
+  if (!std::isfinite(cfg->trust_init) || cfg->trust_init <= 0.0)
+    return fail(GSS_ERR_DOMAIN, "trust_init must be > 0");
+  std::vector<double> zero(static_cast<size_t>(p), 0.0);
+  rc = gss_engine_load_beta(E, zero.data(), p);  // ccd.cpp:137
+  if (rc) return rc;
+  cudaStream_t s = E->stream;
+  {
+    std::vector<double> hw(static_cast<size_t>(p), cfg->trust_init);
+    std::vector<uint8_t> pz(static_cast<size_t>(p), 0);
+    for (int64_t j = 0; j < p; ++j)
+      pz[j] = (pen->kind != GSS_PEN_NONE && !(pen->exempt && pen->exempt[j])) ? 1 : 0;
+    if (p) {
+      GSS_CUDA(cudaMemcpyAsync(E->halfwidth, hw.data(), p * sizeof(double), cudaMemcpyHostToDevice, s));
+      GSS_CUDA(cudaMemcpyAsync(E->penalized, pz.data(), p, cudaMemcpyHostToDevice, s));
+    }
+    GSS_CUDA(cudaStreamSynchronize(s));
+  }
+  E->prm.pen_kind = pen->kind;
+  E->prm.pen_strength = pen->strength;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  E->h_ctl->skipped = 0;
+  E->h_ctl->pend_col = -1;
+  E->h_ctl->pend_delta = 0.0;
+  E->h_ctl->refresh_pending = 0;
+  E->h_ctl->halted = 0;
+  E->h_ctl->err_code = 0;
+  rc = push_ctl(E);
+  if (rc) return rc;
+
+  *res = gss_fit_result{};
+  double ll = 0.0;
+  rc = gss_engine_log_likelihood(E, &ll);
+  if (rc) return rc;
+  double prev = ll - penalty_value(pen, E->h_beta);
+  if (trace_out) trace_out[0] = prev;
+  bool converged = p == 0;
+
+  // capture one cycle: p fused coordinate sweeps + the objective sweep
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (!converged) {
+    GSS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int64_t j = 0; j < p; ++j) {
+      E->prm.column = j;
+      cudaError_t le = launch_sweep(kModeGradCcd, &E->tm_e, &E->tm_code, E->prm, E->grid, s);
+      if (le != cudaSuccess) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        return fail(GSS_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(le));
+      }
+    }
+    E->prm.column = 0;
+    GSS_CUDA(launch_sweep(kModeLoglik, &E->tm_e, &E->tm_code, E->prm, E->grid, s));
+    GSS_CUDA(cudaStreamEndCapture(s, &graph));
+    GSS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  double dev_ms = 0.0;
+  int64_t cycle = 0;
+  int err = GSS_OK;
+  for (cycle = 1; !converged && cycle <= cfg->max_cycles; ++cycle) {
+    cudaEventRecord(E->ev0, s);
+    cudaError_t le = cudaGraphLaunch(exec, s);
+    cudaEventRecord(E->ev1, s);
+    if (le != cudaSuccess) {
+      err = fail(GSS_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(le));
+      break;
+    }
+    err = sync_ctl(E);
+    if (err) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, E->ev0, E->ev1);
+    dev_ms += ms;
+    if (E->h_ctl->err_code) {
+      // keep the device beta (already-accepted updates) visible to the caller
+      cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
+      err = device_error(E, "fit");
+      break;
+    }
+    res->cycles = cycle;
+    if (p) cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
+    const double obj = E->h_ctl->loglik - penalty_value(pen, E->h_beta);
+    if (trace_out) trace_out[cycle] = obj;
+    if (obj < prev - 1e-10) ++res->monotonicity_violations;
+    if (std::abs(obj - prev) / std::max(1.0, std::abs(obj)) < cfg->tolerance) converged = true;
+    prev = obj;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  E->last_ms = dev_ms;
+  E->last_launches = res->cycles * (p + 1);
+  if (err) return err;
+  res->converged = converged ? 1 : 0;
+  res->objective = prev;
+  res->skipped_steps = E->h_ctl->skipped;
+  res->nonzero_count = 0;
+  for (int64_t j = 0; j < p; ++j) res->nonzero_count += E->h_beta[j] != 0.0;
+  if (beta_out) std::copy(E->h_beta.begin(), E->h_beta.end(), beta_out);
+  res->device_seconds = dev_ms * 1e-3;
+  res->wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return GSS_OK;
+}
+
+int gss_engine_max_abs_gradient(gss_engine* E, double* out) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  double top = 0.0;
+  for (int64_t j = 0; j < E->ds->p; ++j) {
+    double g = 0.0;
+    rc = gss_engine_grad_hessian(E, j, &g, nullptr, nullptr);
+    if (rc) return rc;
+    top = std::max(top, std::abs(g));
+  }
+  *out = top;
+  return GSS_OK;
+}
+
+int gss_engine_last_timing(gss_engine* E, double* scan_ms, int64_t* launches) {
+  if (!E) return fail(GSS_ERR_DOMAIN, "null engine");
+  if (scan_ms) *scan_ms = E->last_ms;
+  if (launches) *launches = E->last_launches;
+  return GSS_OK;
+}
+
+}  // extern "C"

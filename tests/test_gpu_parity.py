@@ -1,0 +1,177 @@
+"""Device path vs the reference (golden fixtures) and the pinned C oracle.
+
+All calls go through the C ABI (libgss.so, include/gss.h).  Tolerances are
+the north star's (BASELINE.json): 1e-10 relative on log-likelihood, gradient
+and Hessian; 1e-8 on fitted coefficients.  Gradients use the
+conditioning-aware denominator of SURVEY.md §8a (tests/_common.py).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests._common import TOL_BETA, TOL_DERIV, cases, fit_cases, load, raw, rel, rel_cond
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi():
+    from paper_2204_08183_b200 import capi as C
+    assert C.lib().gss_device_count() > 0
+    return C
+
+
+def _sorted(c):
+    args, strata = raw(c)
+    return orc.assemble(*args, strata=strata)
+
+
+COX = [n for n in cases() if not n.startswith("ka_") and str(load(n)["model"]) == "cox"]
+
+
+@pytest.mark.parametrize("name", cases("ka_"))
+def test_known_answers(capi, name):
+    c = load(name)
+    ds = _sorted(c)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    gh = eng.grad_hessian(0)
+    assert gh["gradient"] == pytest.approx(float(c["grad0"][0]), abs=1e-15)
+    assert gh["hessian"] == pytest.approx(float(c["hess0"][0]), abs=1e-15)
+    assert eng.log_likelihood() == pytest.approx(float(c["ll0"]), rel=1e-15, abs=1e-15)
+
+
+@pytest.mark.parametrize("name", COX)
+def test_derivatives_vs_reference(capi, name):
+    c = load(name)
+    ds = _sorted(c)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    assert rel(eng.log_likelihood(), c["ll0"]) < TOL_DERIV
+    eng.load_beta(c["beta_probe"])
+    assert rel(eng.log_likelihood(), c["ll"]) < TOL_DERIV
+    for j in range(ds.p):
+        gh = eng.grad_hessian(j)
+        assert rel_cond(gh["gradient"], c["grad"][j], gh["fixed_term"]) < TOL_DERIV, j
+        assert rel(gh["hessian"], c["hess"][j]) < TOL_DERIV, j
+
+
+@pytest.mark.parametrize("name", COX)
+def test_fits_vs_reference(capi, name):
+    c = load(name)
+    ds = _sorted(c)
+    dd = capi.Dataset.from_sorted(ds)
+    max_cycles = 200 if "strata" in c else 1000
+    for k, pen, lam in fit_cases(c):
+        eng = capi.Engine(dd, "cox")
+        r = eng.fit(penalty=pen, strength=lam, max_cycles=max_cycles)
+        assert r["cycles"] == int(c[f"fit{k}_cycles"]), (pen, lam)
+        assert np.max(rel(r["beta"], c[f"fit{k}_beta"])) < TOL_BETA, (pen, lam)
+        assert rel(r["objective"], c[f"fit{k}_objective"]) < TOL_DERIV
+        assert np.max(rel(r["objective_trace"], c[f"fit{k}_trace"])) < TOL_DERIV
+
+
+def _random_sorted(n, p, density, seed, quant=None, strata=None, valued=False):
+    rng = np.random.default_rng(seed)
+    nnz_per_col = rng.binomial(n, density, size=p)
+    rows, cols, vals = [], [], []
+    for j, k in enumerate(nnz_per_col):
+        r = rng.choice(n, size=k, replace=False)
+        rows.append(r)
+        cols.append(np.full(k, j))
+        vals.append(np.round(rng.normal(size=k), 3) if valued else np.ones(k))
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    vals = np.concatenate(vals)
+    vals[vals == 0] = 0.5
+    t = rng.exponential(size=n)
+    if quant:
+        t = np.ceil(t * quant) / quant
+    status = (rng.random(n) < 0.7).astype(np.int64)
+    st = None if strata is None else rng.integers(0, strata, size=n)
+    return orc.assemble(t, status, rows, cols, vals, p, strata=st)
+
+
+@pytest.mark.parametrize("n,p,quant,strata,valued", [
+    (100_000, 24, None, None, False),
+    (150_001, 16, 100.0, None, False),
+    (60_000, 12, 30.0, 7, False),
+    (70_000, 10, None, None, True),
+])
+def test_multitile_vs_oracle(capi, n, p, quant, strata, valued):
+    ds = _random_sorted(n, p, 0.02, seed=n + p, quant=quant, strata=strata, valued=valued)
+    ref = orc.OracleEngine(ds, "cox")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    beta = np.random.default_rng(3).uniform(-0.4, 0.4, size=p)
+    ref.load_beta(beta)
+    eng.load_beta(beta)
+    assert np.max(rel(eng.xbeta(), ref.eta[:n])) < 1e-13
+    assert rel(eng.log_likelihood(), ref.log_likelihood()) < TOL_DERIV
+    for j in range(p):
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        assert rel_cond(a["gradient"], b["gradient"], b["fixed_term"]) < TOL_DERIV
+        assert rel(a["hessian"], b["hessian"]) < TOL_DERIV
+    # fit parity at a fixed number of cycles (convergence tests a rounded objective)
+    eng2 = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    ref2 = orc.OracleEngine(ds, "cox")
+    r1 = eng2.fit(penalty="l1", strength=2.0, max_cycles=6)
+    r2 = ref2.fit(penalty="l1", strength=2.0, max_cycles=6)
+    assert r1["cycles"] == r2["cycles"]
+    assert np.max(rel(r1["beta"], r2["beta"])) < TOL_BETA
+    assert np.max(rel(r1["objective_trace"], r2["objective_trace"])) < TOL_DERIV
+
+
+def test_row_mask_equals_subset(capi):
+    """A masked engine behaves exactly like the subset_rows() dataset
+    (src/dataset.cpp:268-322) — the CV fold representation."""
+    ds = _random_sorted(30_000, 8, 0.05, seed=5, quant=20.0)
+    mask = (np.random.default_rng(1).random(ds.n) < 0.8).astype(np.uint8)
+    keep = np.nonzero(mask)[0]
+    # subset in sorted order with fresh ids preserving the order
+    sub_rows = np.repeat(np.arange(ds.p), np.diff(ds.col_ptr))
+    remap = -np.ones(ds.n, np.int64)
+    remap[keep] = np.arange(len(keep))
+    sel = remap[ds.row_idx] >= 0
+    sub = orc.assemble(ds.times[keep], ds.status[keep], remap[ds.row_idx[sel]], sub_rows[sel],
+                       ds.vals[sel], ds.p)
+    ref = orc.OracleEngine(sub, "cox")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox", row_mask=mask)
+    beta = np.linspace(-0.3, 0.3, ds.p)
+    ref.load_beta(beta)
+    eng.load_beta(beta)
+    assert rel(eng.log_likelihood(), ref.log_likelihood()) < TOL_DERIV
+    for j in range(ds.p):
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        assert rel_cond(a["gradient"], b["gradient"], b["fixed_term"]) < TOL_DERIV
+        assert rel(a["hessian"], b["hessian"]) < TOL_DERIV
+
+
+def test_update_semantics_and_refresh(capi):
+    """update_xbeta_sparse: indicator multiply rule, overflow atomicity,
+    refresh cadence (tests/test_engine.cpp:178-263)."""
+    ds = _random_sorted(20_000, 6, 0.05, seed=9, valued=False)
+    ref = orc.OracleEngine(ds, "cox", recompute_interval=3)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox", recompute_interval=3)
+    for j, d in [(0, 0.3), (1, -0.2), (2, 0.1), (0, 0.05), (3, 0.7)]:
+        ref.update(j, d)
+        eng.update(j, d)
+    assert eng.counters() == (5, 1)
+    assert np.max(rel(eng.exp_xbeta(), ref.e[:ds.n])) < 1e-14
+    assert np.max(rel(eng.xbeta(), ref.eta[:ds.n])) < 1e-14
+    before = eng.xbeta()
+    with pytest.raises(capi.GssError) as ei:
+        eng.update(4, 800.0)
+    assert ei.value.kind == "OverflowError"
+    assert np.array_equal(eng.xbeta(), before)
+    with pytest.raises(capi.GssError) as ei:
+        eng.grad_hessian(99)
+    assert ei.value.kind == "InvalidColumnError"
+
+
+def test_determinism(capi):
+    ds = _random_sorted(200_000, 4, 0.01, seed=11, quant=50.0)
+    dd = capi.Dataset.from_sorted(ds)
+    outs = []
+    for _ in range(3):
+        eng = capi.Engine(dd, "cox")
+        eng.load_beta(np.array([0.2, -0.1, 0.3, 0.05]))
+        outs.append([eng.grad_hessian(j)["gradient"] for j in range(4)] + [eng.log_likelihood()])
+    assert outs[0] == outs[1] == outs[2]
