@@ -163,8 +163,12 @@ int gss_engine_fit(gss_engine* e, const gss_penalty_spec* pen, const gss_fit_con
  */
 int gss_engine_max_abs_gradient(gss_engine* e, double* out);
 
-/* Device time (ms) of the last fused coordinate kernel launch set, for bench. */
+/* Device time (ms) of the last fit's coordinate cycles, for bench. */
 int gss_engine_last_timing(gss_engine* e, double* scan_ms, int64_t* launches);
+/* Per-cycle statistics of the last fit: CUDA-event device time of each
+ * cycle's graph (ms) and the accepted-update count after each cycle.
+ * Returns the number of cycles written (<= max). */
+int64_t gss_engine_cycle_stats(gss_engine* e, double* ms, int64_t* accepted, int64_t max);
 
 #ifdef __cplusplus
 }

@@ -129,6 +129,53 @@ class Dataset:
             self.h = None
 
 
+class SimConfig(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("p", ctypes.c_int64), ("density", ctypes.c_double),
+                ("beta_sparsity", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("censoring_quantile", ctypes.c_double), ("time_quantum", ctypes.c_double)]
+
+
+class SimOut(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("p", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("times", ctypes.POINTER(ctypes.c_double)),
+                ("status", ctypes.POINTER(ctypes.c_int32)),
+                ("col_ptr", ctypes.POINTER(ctypes.c_int64)),
+                ("row_idx", ctypes.POINTER(ctypes.c_int32)),
+                ("beta_true", ctypes.POINTER(ctypes.c_double))]
+
+
+class SimData:
+    """Benchmark-scale synthetic design in PINNED host memory (gss_sim.h).
+    Arrays are zero-copy numpy views valid while this object lives."""
+
+    def __init__(self, n, p, density=0.01, beta_sparsity=0.8, seed=0, censoring_quantile=0.0,
+                 time_quantum=0.0, device=0):
+        L = lib()
+        L.gss_sim_last_error.restype = ctypes.c_char_p
+        self._out = SimOut()
+        cfg = SimConfig(n, p, density, beta_sparsity, seed, censoring_quantile, time_quantum)
+        rc = L.gss_simulate_cox(ctypes.byref(cfg), device, ctypes.byref(self._out))
+        if rc:
+            raise GssError(rc, L.gss_sim_last_error().decode())
+        o = self._out
+        self.n, self.p, self.nnz = o.n, o.p, o.nnz
+        as_np = np.ctypeslib.as_array
+        self.times = as_np(o.times, shape=(o.n,))
+        self.status = as_np(o.status, shape=(o.n,))
+        self.col_ptr = as_np(o.col_ptr, shape=(o.p + 1,))
+        self.row_idx = as_np(o.row_idx, shape=(max(o.nnz, 1),))[:o.nnz]
+        self.beta_true = as_np(o.beta_true, shape=(max(o.p, 1),))[:o.p]
+
+    def host_bytes(self):
+        return (self.times.nbytes + self.status.nbytes + self.col_ptr.nbytes
+                + self.row_idx.nbytes)
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "_out", None) is not None:
+            _lib.gss_sim_free(ctypes.byref(self._out))
+            self._out = None
+
+
 class Engine:
     """survscan::Engine surface over the C ABI (engine.hpp:33-90)."""
 
@@ -222,3 +269,11 @@ class Engine:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         check(lib().gss_engine_last_timing(self.h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+    def cycle_stats(self, max_cycles=100000):
+        ms = np.zeros(max_cycles)
+        acc = np.zeros(max_cycles, np.int64)
+        L = lib()
+        L.gss_engine_cycle_stats.restype = ctypes.c_int64
+        k = L.gss_engine_cycle_stats(self.h, _p(ms), _p(acc), ctypes.c_int64(max_cycles))
+        return ms[:k].copy(), acc[:k].copy()

@@ -1,6 +1,7 @@
 // gss_aux.cu — the non-scan kernels of the engine: dataset packing
 // (tile-blocked column pointers, CSR transpose, per-column max |x|), fixed
 // terms, load_beta's full X*beta, and the API-mode validate/commit update.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -194,6 +195,26 @@ __global__ void update_commit_kernel(SweepParams P, int64_t col, double delta, d
     atomicMax(&P.ctl->eta_absmax_bits, static_cast<unsigned long long>(__double_as_longlong(mx)));
 }
 
+// layout contract of the CSC input: indices in [0, n), strictly ascending per column
+__global__ void validate_csc_kernel(const int64_t* __restrict__ col_ptr,
+                                    const int32_t* __restrict__ row_idx, int64_t p, int64_t n,
+                                    int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; j < p;
+       j += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t a = col_ptr[j], b = col_ptr[j + 1];
+    if (b < a) {
+      if (lane == 0) atomicOr(bad, 1);
+      continue;
+    }
+    for (int64_t k = a + lane; k < b; k += 32) {
+      const int32_t r = row_idx[k];
+      if (r < 0 || r >= n) atomicOr(bad, 2);
+      if (k > a && row_idx[k - 1] >= r) atomicOr(bad, 4);
+    }
+  }
+}
+
 int grid_for(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   if (g < 1) g = 1;
@@ -202,6 +223,25 @@ int grid_for(int64_t work, int block) {
 }
 
 }  // namespace
+
+cudaError_t launch_validate_csc(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
+                                int64_t n, int* bad, cudaStream_t s) {
+  if (p == 0) return cudaSuccess;
+  validate_csc_kernel<<<grid_for(p * 32, 256), 256, 0, s>>>(col_ptr, row_idx, p, n, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s);
+  if (e != cudaSuccess) return e;
+  void* tmp = nullptr;
+  e = cudaMallocAsync(&tmp, tb, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, n, s);
+  cudaFreeAsync(tmp, s);
+  return e;
+}
 
 cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s) {

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -129,8 +130,10 @@ struct gss_engine {
   uint32_t* code = nullptr;
   double *beta = nullptr, *halfwidth = nullptr, *fixed = nullptr;
   uint8_t* penalized = nullptr;
-  unsigned long long *statA = nullptr, *statP = nullptr;
-  double *aggA = nullptr, *aggP = nullptr, *tile_part = nullptr;
+  double *agg = nullptr, *prefix = nullptr, *tsum = nullptr, *gsum = nullptr, *gpre = nullptr;
+  unsigned int* grp_cnt = nullptr;
+  int32_t* tile_lastseg = nullptr;
+  double* tile_part = nullptr;
   Ctl* ctl = nullptr;
   int* dflag = nullptr;
   Ctl* h_ctl = nullptr;  // pinned mirror
@@ -139,13 +142,15 @@ struct gss_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
+  std::vector<double> cycle_ms;
+  std::vector<int64_t> cycle_accepted;
 
   ~gss_engine() {
     cudaSetDevice(ds->device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)u, (void*)g, (void*)code,
-                    (void*)beta, (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)statA,
-                    (void*)statP, (void*)aggA, (void*)aggP, (void*)tile_part, (void*)ctl,
+                    (void*)beta, (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)agg, (void*)gsum, (void*)gpre, (void*)grp_cnt,
+                    (void*)prefix, (void*)tsum, (void*)tile_lastseg, (void*)tile_part, (void*)ctl,
                     (void*)dflag})
       if (q) cudaFree(q);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -356,15 +361,7 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     if (i > 0 && !new_stratum && h->times[i] > h->times[i - 1])
       return fail(GSS_ERR_DOMAIN, "rows must be sorted by decreasing time within a stratum");
   }
-  for (int64_t j = 0; j < p; ++j) {
-    if (h->col_ptr[j + 1] < h->col_ptr[j]) return fail(GSS_ERR_DOMAIN, "col_ptr not monotone");
-    for (int64_t k = h->col_ptr[j]; k < h->col_ptr[j + 1]; ++k) {
-      if (h->row_idx[k] < 0 || h->row_idx[k] >= n)
-        return fail(GSS_ERR_INDEX, "row index outside [0, n)");
-      if (k > h->col_ptr[j] && h->row_idx[k] <= h->row_idx[k - 1])
-        return fail(GSS_ERR_DOMAIN, "row indices must strictly ascend within a column");
-    }
-  }
+  if (p > 0 && h->col_ptr[0] != 0) return fail(GSS_ERR_DOMAIN, "col_ptr[0] must be 0");
   auto* ds = new gss_dataset();
   ds->device = device;
   ds->n = n;
@@ -429,6 +426,19 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   if (p) PK(cudaMemcpyAsync(ds->col_ind, ind.data(), p, cudaMemcpyHostToDevice, s));
   if (ds->has_vals && nnz)
     PK(cudaMemcpyAsync(ds->vals, h->vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  {
+    int* bad = nullptr;
+    PK(dalloc(&bad, 1));
+    PK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    PK(launch_validate_csc(ds->col_ptr, ds->row_idx, p, n, bad, s));
+    int hb = 0;
+    PK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PK(cudaStreamSynchronize(s));
+    cudaFree(bad);
+    if (hb & 2) return cleanup(fail(GSS_ERR_INDEX, "row index outside [0, n)"));
+    if (hb) return cleanup(fail(GSS_ERR_DOMAIN, "CSC columns must have monotone col_ptr and "
+                                                "strictly ascending row indices"));
+  }
   if (p) {
     PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
     PK(launch_colmax(ds->col_ptr, ds->has_vals ? ds->vals : nullptr, p, ds->colmax, s));
@@ -439,14 +449,8 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     PK(dalloc(&cnt, n + 1));
     PK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int64_t), s));
     PK(launch_csr_count(ds->row_idx, nnz, cnt, s));
-    std::vector<int64_t> hc(static_cast<size_t>(n + 1), 0);
-    PK(cudaMemcpyAsync(hc.data(), cnt, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    PK(cudaStreamSynchronize(s));
-    std::vector<int64_t> rp(static_cast<size_t>(n + 1), 0);
-    for (int64_t i = 0; i < n; ++i) rp[i + 1] = rp[i] + hc[i];
-    PK(cudaMemcpyAsync(ds->row_ptr, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                       s));
-    PK(cudaMemcpyAsync(cnt, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    PK(launch_exclusive_scan(cnt, ds->row_ptr, n + 1, s));
+    PK(cudaMemcpyAsync(cnt, ds->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     PK(launch_csr_fill(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, p, cnt,
                        ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
     PK(launch_csr_sort_rows(ds->row_ptr, n, ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
@@ -513,10 +517,14 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(dalloc(&E->halfwidth, p));
   EK(dalloc(&E->fixed, p));
   EK(dalloc(&E->penalized, p));
-  EK(dalloc(&E->statA, nt));
-  EK(dalloc(&E->statP, ng));
-  EK(dalloc(&E->aggA, size_t(nt) * 8));
-  EK(dalloc(&E->aggP, size_t(ng) * 8));
+  EK(dalloc(&E->agg, size_t(nt) * 4));
+  EK(dalloc(&E->prefix, size_t(nt) * 4));
+  EK(dalloc(&E->tsum, size_t(nt) * 4));
+  EK(dalloc(&E->gsum, size_t(nt / 32 + 1) * 4));
+  EK(dalloc(&E->gpre, size_t(nt / 32 + 1) * 4));
+  EK(dalloc(&E->grp_cnt, size_t(nt / 32 + 1)));
+  EK(cudaMemsetAsync(E->grp_cnt, 0, size_t(nt / 32 + 1) * sizeof(unsigned), E->stream));
+  EK(dalloc(&E->tile_lastseg, nt));
   EK(dalloc(&E->tile_part, size_t(nt) * 4));
   EK(dalloc(&E->ctl, 1));
   EK(dalloc(&E->dflag, 4));
@@ -535,8 +543,14 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
     EK(cudaStreamSynchronize(s));
   }
   EK(cudaMemsetAsync(E->beta, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
-  EK(cudaMemsetAsync(E->statA, 0, nt * sizeof(unsigned long long), s));
-  EK(cudaMemsetAsync(E->statP, 0, ng * sizeof(unsigned long long), s));
+
+  {
+    std::vector<int32_t> ls(static_cast<size_t>(nt), -1);
+    for (int64_t i = 0; i < npad; ++i)
+      if (E->h_code[i] & kCodeSeg) ls[i / kTileRows] = static_cast<int32_t>(i % kTileRows);
+    EK(cudaMemcpyAsync(E->tile_lastseg, ls.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    EK(cudaStreamSynchronize(s));
+  }
   EK(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   EK(launch_fixed_terms(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, ds->col_ind,
                         E->code, p, E->fixed, s));
@@ -581,13 +595,28 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.weighted = E->weighted ? 1 : 0;
   P.pen_strength = 0.0;
   P.recompute_interval = recompute_interval;
-  P.statA = E->statA;
-  P.aggA = E->aggA;
-  P.statP = E->statP;
-  P.aggP = E->aggP;
+  P.agg = E->agg;
+  P.prefix = E->prefix;
+  P.tsum = E->tsum;
+  P.gsum = E->gsum;
+  P.gpre = E->gpre;
+  P.grp_cnt = E->grp_cnt;
+  P.has_mask = row_mask ? 1 : 0;
+  P.has_strata = 0;
+  for (int64_t i = 1; i < n; ++i)
+    if (E->h_code[i] & kCodeSeg) P.has_strata = 1;
+  P.tile_lastseg = E->tile_lastseg;
   P.tile_part = E->tile_part;
   P.ctl = E->ctl;
   P.column = 0;
+  if (const char* tr = std::getenv("GSS_TRACE")) {
+    if (tr[0] == '1') {
+      P.trace_cap = 1u << 22;
+      EK(dalloc(&P.trace, size_t(P.trace_cap) * 2));
+      EK(dalloc(&P.trace_n, 1));
+      EK(cudaMemset(P.trace_n, 0, sizeof(unsigned)));
+    }
+  }
 #undef EK
   *out = E;
   return GSS_OK;
@@ -608,6 +637,13 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
   GSS_CUDA(dalloc(&dbeta, p));
   cudaStream_t s = E->stream;
   if (p) GSS_CUDA(cudaMemcpyAsync(dbeta, beta, p * sizeof(double), cudaMemcpyHostToDevice, s));
+  {
+    int rc2 = sync_ctl(E);
+    if (rc2) {
+      cudaFree(dbeta);
+      return rc2;
+    }
+  }
   GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
   GSS_CUDA(launch_spmv_rows(E->prm, dbeta, E->scratch, E->dflag, s));
   int over = 0;
@@ -618,6 +654,11 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
     return fail(GSS_ERR_OVERFLOW, "load_beta: |x'beta| exceeds 700");
   }
   if (p) GSS_CUDA(cudaMemcpyAsync(E->beta, dbeta, p * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  E->h_ctl->tprev_valid = 0;      // e rewritten outside a sweep: per-tile sums stale
+  E->h_ctl->eta_absmax_bits = 0;  // fresh eta: the bound is rebuilt exactly by the commit
+  E->h_ctl->absmax_next_bits = 0;
+  E->h_ctl->bound_slack = 0.0;
+  GSS_CUDA(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   GSS_CUDA(launch_commit_eta(E->prm, E->scratch, s));
   GSS_CUDA(cudaStreamSynchronize(s));
   cudaFree(dbeta);
@@ -659,6 +700,7 @@ int gss_engine_update(gss_engine* E, int64_t column, double delta) {
   rc = sync_ctl(E);
   if (rc) return rc;
   E->h_ctl->accepted += 1;
+  E->h_ctl->tprev_valid = 0;  // e changed outside a sweep
   const bool refresh = E->h_ctl->accepted % E->interval == 0;
   rc = push_ctl(E);
   if (rc) return rc;
@@ -822,6 +864,8 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
     GSS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   }
   double dev_ms = 0.0;
+  E->cycle_ms.clear();
+  E->cycle_accepted.clear();
   int64_t cycle = 0;
   int err = GSS_OK;
   for (cycle = 1; !converged && cycle <= cfg->max_cycles; ++cycle) {
@@ -837,6 +881,8 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
     float ms = 0.f;
     cudaEventElapsedTime(&ms, E->ev0, E->ev1);
     dev_ms += ms;
+    E->cycle_ms.push_back(ms);
+    E->cycle_accepted.push_back(E->h_ctl->accepted);
     if (E->h_ctl->err_code) {
       // keep the device beta (already-accepted updates) visible to the caller
       cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
@@ -887,6 +933,27 @@ int gss_engine_last_timing(gss_engine* E, double* scan_ms, int64_t* launches) {
   if (scan_ms) *scan_ms = E->last_ms;
   if (launches) *launches = E->last_launches;
   return GSS_OK;
+}
+
+// Debug: copy the event trace (GSS_TRACE=1) to host; returns events copied.
+int64_t gss_engine_trace(gss_engine* E, unsigned long long* out, int64_t max_events) {
+  if (!E || !E->prm.trace) return 0;
+  unsigned n = 0;
+  cudaMemcpy(&n, E->prm.trace_n, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  const int64_t k = std::min<int64_t>(std::min<int64_t>(n, E->prm.trace_cap), max_events);
+  cudaMemcpy(out, E->prm.trace, size_t(k) * 16, cudaMemcpyDeviceToHost);
+  cudaMemset(E->prm.trace_n, 0, sizeof(unsigned));
+  return k;
+}
+
+int64_t gss_engine_cycle_stats(gss_engine* E, double* ms, int64_t* accepted, int64_t max) {
+  if (!E) return 0;
+  const int64_t k = std::min<int64_t>(max, static_cast<int64_t>(E->cycle_ms.size()));
+  for (int64_t i = 0; i < k; ++i) {
+    if (ms) ms[i] = E->cycle_ms[i];
+    if (accepted) accepted[i] = E->cycle_accepted[i];
+  }
+  return k;
 }
 
 }  // extern "C"

@@ -16,10 +16,10 @@ constexpr int kIpt = 8;                    // rows per consumer thread
 constexpr int kTileRows = kThreads * kIpt; // 2048 rows per tile
 constexpr int kProducerWarps = 1;
 constexpr int kCtaThreads = kThreads + 32 * kProducerWarps;
-constexpr int kGroup = 256;                // look-back checkpoint group (tiles)
-constexpr int kNnzCap = 512;               // per-stage smem capacity of a column's
+constexpr int kGroup = 128;                // look-back group (tiles) with a published aggregate
+constexpr int kNnzCap = 256;               // per-stage smem capacity of a column's
                                            // in-tile nonzero list (ints)
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 
 // per-row code word (int32): built per engine from times/status/mask/strata
 constexpr uint32_t kCodeCount = 0x1FFFFFFFu;  // events in the tied block, at its last row

@@ -10,9 +10,14 @@ namespace gss {
 
 // Per-engine device control block (zero-initialised at engine creation).
 struct Ctl {
-  // look-back / tail protocol
-  unsigned int tile_counter;   // dynamic tile ids
-  unsigned int ticket;         // CTA completion count (last CTA runs the tail)
+  // contended words each own a 128-byte line (atomics vs. polling)
+  alignas(128) unsigned int tile_counter;   // dynamic tile ids (phase C)
+  alignas(128) unsigned int ticket;         // CTA completion count (last CTA runs the tail)
+  alignas(128) unsigned int items_a;        // phase-A work items claimed
+  alignas(128) unsigned int groups_done;    // 32-tile groups scanned (last one scans groups)
+  alignas(128) unsigned long long ready;    // epoch whose tile prefixes are published
+  alignas(128) int tprev_valid;             // tsum holds fresh per-tile sums of the current e
+  int pad2;
   unsigned long long epoch;    // launch generation tag for tile status words
   // deferred state change applied by the NEXT sweep's tile phase
   long long pend_col;          // -1: none
@@ -23,7 +28,9 @@ struct Ctl {
   int err_code;                // gss_status of the first error in the cycle
   int pad0;
   long long err_col;
-  unsigned long long eta_absmax_bits;  // conservative bound on max |eta| (double bits)
+  unsigned long long eta_absmax_bits;  // max |eta| at the last refresh/load (double bits)
+  unsigned long long absmax_next_bits; // max |eta| gathered by a refresh sweep in flight
+  double bound_slack;                  // sum |delta| * max|x| of updates since then
   long long accepted;          // Engine::accepted_ (engine.hpp:88)
   long long refreshes;         // Engine::refreshes_
   long long skipped;           // FitResult.skipped_steps (ccd.cpp:161-164)
@@ -65,22 +72,34 @@ struct SweepParams {
   int weighted;
   double pen_strength;
   long long recompute_interval;
-  // look-back scratch
-  unsigned long long* statA;   // [ntiles]
-  double* aggA;                // [ntiles][4]
-  unsigned long long* statP;   // [ngroups]
-  double* aggP;                // [ngroups][4]
+  // carry scratch
+  double* agg;                 // [ntiles][4] phase-A tile aggregates (f, a, b, c)
+  double* prefix;              // [ntiles][4] exclusive tile prefixes inside the 32-tile group
+  double* gsum;                // [ngroups][4] group totals
+  double* gpre;                // [ngroups][4] exclusive group prefixes
+  unsigned int* grp_cnt;       // [ngroups] phase-A tiles completed per group (reset by the tail)
+  double* tsum;                // [2][ntiles][2] fresh per-tile (f, sum e) by launch parity
+  const int32_t* tile_lastseg; // [ntiles] last stratum-start row in the tile, -1 if none
+  int has_mask;                // some rows are masked out (row_mask engine)
+  int has_strata;              // a stratum starts after row 0 (segmented scan needed)
   double* tile_part;           // [ntiles][4]
   Ctl* ctl;
   int64_t column;              // scan column for grad modes
+  unsigned long long* trace;   // optional event trace [cap][2] (GSS_TRACE=1), else null
+  unsigned int* trace_n;
+  unsigned int trace_cap;
 };
 
 // launchers (gss_kernels.cu)
 cudaError_t launch_sweep(int mode, const CUtensorMap* tm_e, const CUtensorMap* tm_code,
                          const SweepParams& prm, int grid, cudaStream_t s);
 int sweep_max_active_ctas_per_sm();
+int sweep_threads();
 size_t sweep_smem_bytes();
 
+cudaError_t launch_validate_csc(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
+                                int64_t n, int* bad, cudaStream_t s);
+cudaError_t launch_exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
 cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s);
 cudaError_t launch_colmax(const int64_t* col_ptr, const double* vals, int64_t p,
