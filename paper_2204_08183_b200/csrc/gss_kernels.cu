@@ -51,7 +51,7 @@ constexpr int kConsumerWarps = kThreads / 32;  // 8
 constexpr int kProducerWarp = kConsumerWarps;   // 8
 constexpr int kWarps = kConsumerWarps + 1;
 constexpr int kSweepThreads = 32 * kWarps;      // 288
-constexpr int kScratchInts = 512;               // per-warp phase-A scratch (smem)
+constexpr int kScratchInts = 128;               // per-warp phase-A scratch (smem)
 constexpr double kXbetaBound = 700.0;           // src/engine.cpp:12
 constexpr double kHwFloor = 1e-300;             // src/ccd.cpp:13
 constexpr double kFastBound = 700.0 * (1.0 - 1e-12);
@@ -72,14 +72,13 @@ struct SmemTail {
   double scan[2][kConsumerWarps][4];  // block-scan warp totals, double-buffered by tile parity
   double part[2][kConsumerWarps][4];  // per-warp tile partials, double-buffered by tile parity
   double bcast[8];
+  int32_t scratch[kConsumerWarps][kScratchInts];  // phase-A pending-column lists
   int flag;
 };
 
 __host__ __device__ constexpr size_t smem_total() {
   return 1024 /*align slack*/ + size_t(kStages) * kStageBytes + sizeof(SmemTail);
 }
-static_assert(size_t(kWarps) * kScratchInts * 4 <= size_t(kStages) * kStageBytes,
-              "phase-A scratch lives in the (not yet used) stage buffers");
 
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
@@ -401,14 +400,30 @@ __device__ void group_scan(const SweepParams& P, int g, int gsize, int lane) {
 __device__ void final_scan(const SweepParams& P, int ng, int lane) {
   const int per = (ng + 31) / 32;
   const int g0 = min(ng, lane * per), g1 = min(ng, g0 + per);
+  // loads batched 8 at a time (independent), folded in order
+  constexpr int kB = 8;
   Seg<3> own = Seg<3>::zero();
-  for (int g = g0; g < g1; ++g) own = seg_combine(own, load_seg(P.gsum + size_t(g) * 4));
+  for (int b = g0; b < g1; b += kB) {
+    Seg<3> x[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      x[q] = b + q < g1 ? load_seg(P.gsum + size_t(b + q) * 4) : Seg<3>::zero();
+#pragma unroll
+    for (int q = 0; q < kB; ++q) own = seg_combine(own, x[q]);
+  }
   const Seg<3> inc = warp_inclusive_scan(own, lane);
   Seg<3> run = shfl_up_seg(inc, 1);
   if (lane == 0) run = Seg<3>::zero();
-  for (int g = g0; g < g1; ++g) {
-    store_seg(P.gpre + size_t(g) * 4, run);
-    run = seg_combine(run, load_seg(P.gsum + size_t(g) * 4));
+  for (int b = g0; b < g1; b += kB) {
+    Seg<3> x[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      x[q] = b + q < g1 ? load_seg(P.gsum + size_t(b + q) * 4) : Seg<3>::zero();
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (b + q < g1) store_seg(P.gpre + size_t(b + q) * 4, run);
+      run = seg_combine(run, x[q]);
+    }
   }
 }
 
@@ -471,34 +486,19 @@ __device__ __forceinline__ void consume(const SweepParams& P, const Pending& pd,
     const int32_t* nnz_s = reinterpret_cast<const int32_t*>(sb + kEBytes + kCodeBytes);
     const int32_t* nnz_u = nnz_s + kNnzCap;
     const int lr0 = tid * kIpt;
-    // prefix loads issued early (latency overlaps the local pass)
-    double pre[1 + L];
+    // prefix loads issued early; consumed only after the block scan, so their
+    // latency overlaps the local pass (raw values, no arithmetic here)
+    double pg[1 + L], pq[1 + L];
     auto load_prefix = [&]() {
       const double* g = P.gpre + size_t(t / 32) * 4;
       const double* q = P.prefix + size_t(t) * 4;
 #pragma unroll
-      for (int i = 0; i < L; ++i) pre[1 + i] = __dadd_rn(__ldcg(g + 1 + i), 0.0);
-      pre[0] = STRATA ? __ldcg(g) : 0.0;
-      // combined below once both halves are needed: keep the in-group half
-      // in the same registers by folding now (pure sums, no select) unless
-      // strata need the segmented rule
-      if constexpr (!STRATA) {
-#pragma unroll
-        for (int i = 0; i < L; ++i) pre[1 + i] = __dadd_rn(pre[1 + i], __ldcg(q + 1 + i));
-      } else {
-        Seg<L> a, b;
-        a.f = pre[0] != 0.0 ? 1u : 0u;
-        b.f = __ldcg(q) != 0.0 ? 1u : 0u;
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-          a.v[i] = pre[1 + i];
-          b.v[i] = __ldcg(q + 1 + i);
-        }
-        const Seg<L> c = seg_combine(a, b);
-        pre[0] = c.f ? 1.0 : 0.0;
-#pragma unroll
-        for (int i = 0; i < L; ++i) pre[1 + i] = c.v[i];
+      for (int i = 0; i < L; ++i) {
+        pg[1 + i] = __ldcg(g + 1 + i);
+        pq[1 + i] = __ldcg(q + 1 + i);
       }
+      pg[0] = STRATA ? __ldcg(g) : 0.0;
+      pq[0] = STRATA ? __ldcg(q) : 0.0;
     };
     if (ready_seen) load_prefix();
 
@@ -639,11 +639,15 @@ __device__ __forceinline__ void consume(const SweepParams& P, const Pending& pd,
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&st->empty[s]);  // stage may be refilled now
-    Seg<L> run;
-    run.f = STRATA ? (pre[0] != 0.0 ? 1u : 0u) : 0u;
+    Seg<L> run, rq;
+    run.f = STRATA ? (pg[0] != 0.0 ? 1u : 0u) : 0u;
+    rq.f = STRATA ? (pq[0] != 0.0 ? 1u : 0u) : 0u;
 #pragma unroll
-    for (int i = 0; i < L; ++i) run.v[i] = pre[1 + i];
-    run = comb<L, STRATA>(run, excl);
+    for (int i = 0; i < L; ++i) {
+      run.v[i] = pg[1 + i];
+      rq.v[i] = pq[1 + i];
+    }
+    run = comb<L, STRATA>(comb<L, STRATA>(run, rq), excl);
 
     // ---- transform at tied-block ends and reduce ----
     double acc0 = 0.0, acc1 = 0.0;
@@ -730,8 +734,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2)
   if (tid == 0) trace_ev(P, 0, 0);
 
   // ------------------------------ phase A ------------------------------------
-  {
-    int32_t* scratch = reinterpret_cast<int32_t*>(smem) + warp * kScratchInts;
+  // consumer warps only: the producer starts streaming tiles immediately
+  if (warp != kProducerWarp) {
+    int32_t* scratch = st->scratch[warp];
     double absmax = 0.0;
     for (;;) {
       unsigned t = 0;
@@ -787,7 +792,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2)
                   static_cast<unsigned long long>(__double_as_longlong(absmax)));
     }
   }
-  __syncthreads();  // phase-A scratch (stage buffers) free again
   if (tid == 0) trace_ev(P, 1, 0);
 
   // ------------------------------ phase C ------------------------------------
