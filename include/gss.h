@@ -149,14 +149,22 @@ typedef struct gss_fit_result {
 
 /*
  * fit_with_engine (src/ccd.cpp:131-184) with the per-coordinate work on the
- * device: each cycle is one CUDA graph of p fused kernels (pending sparse
- * update + scan/transform/reduce + coordinate_step), then one log-likelihood
- * kernel; the host syncs once per cycle to test convergence.
+ * device: each cycle is ONE persistent kernel launch that walks the p
+ * coordinates (scan/transform/reduce + coordinate_step + deferred sparse
+ * update, one grid-wide exchange per coordinate) and then evaluates the
+ * log-likelihood; the host syncs once per cycle to test convergence.
  * beta_out: [p]; trace_out: [max_cycles+1] (may be NULL).
  */
 int gss_engine_fit(gss_engine* e, const gss_penalty_spec* pen, const gss_fit_config* cfg,
                    double* beta_out, double* trace_out, gss_fit_result* out);
 
+/*
+ * Engine::grad_hessian for every column at the engine's current beta in ONE
+ * device launch (the batched sweep behind gamma_max, src/crossval.cpp:104-110).
+ * Each output is [p] (any may be NULL).
+ */
+int gss_engine_grad_hessian_all(gss_engine* e, double* gradient, double* hessian,
+                                double* fixed_term);
 /*
  * gamma_max helper (src/crossval.cpp:104-110): max_j |g'_j| at the engine's
  * current beta, all columns in one batched device sweep.

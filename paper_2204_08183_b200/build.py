@@ -38,9 +38,10 @@ def _run(cmd):
 def build_libgss(force=False):
     cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "gss.h")]
-    if force or _newer(LIBGSS, deps):
+    extra = ["-DGSS_ENABLE_TRACE=1"] if os.environ.get("GSS_TRACE_BUILD") == "1" else []
+    if force or extra or _newer(LIBGSS, deps):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-diag-suppress", "177", "-shared", *cu, "-o", LIBGSS])
+              "-diag-suppress", "177", *extra, "-shared", *cu, "-o", LIBGSS])
     return LIBGSS
 
 

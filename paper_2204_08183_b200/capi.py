@@ -28,7 +28,8 @@ EXPORTS = [
     "gss_engine_grad_hessian", "gss_engine_log_likelihood", "gss_engine_get_beta",
     "gss_engine_get_xbeta", "gss_engine_get_exp_xbeta", "gss_engine_get_fixed_terms",
     "gss_engine_get_ipcw", "gss_engine_counters", "gss_engine_fit",
-    "gss_engine_max_abs_gradient", "gss_engine_last_timing",
+    "gss_engine_max_abs_gradient", "gss_engine_last_timing", "gss_engine_grad_hessian_all",
+    "gss_engine_cycle_stats",
 ]
 
 
@@ -238,6 +239,12 @@ class Engine:
         a, r = ctypes.c_int64(), ctypes.c_int64()
         check(lib().gss_engine_counters(self.h, ctypes.byref(a), ctypes.byref(r)))
         return a.value, r.value
+
+    def grad_hessian_all(self):
+        """All columns at the current beta in one device launch."""
+        g, h, f = np.empty(self.ds.p), np.empty(self.ds.p), np.empty(self.ds.p)
+        check(lib().gss_engine_grad_hessian_all(self.h, _p(g), _p(h), _p(f)))
+        return {"gradient": g, "hessian": h, "fixed_term": f}
 
     def max_abs_gradient(self):
         out = ctypes.c_double()

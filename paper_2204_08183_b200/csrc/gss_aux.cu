@@ -38,6 +38,14 @@ __global__ void tile_ptr_kernel(const int64_t* __restrict__ col_ptr,
   }
 }
 
+// device row positions of the padded (stratum-aligned) layout
+__global__ void remap_rows_kernel(int32_t* __restrict__ row_idx, int64_t nnz,
+                                  const int64_t* __restrict__ dev_row) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x)
+    row_idx[k] = static_cast<int32_t>(dev_row[row_idx[k]]);
+}
+
 // warp per column
 __global__ void colmax_kernel(const int64_t* __restrict__ col_ptr, const double* __restrict__ vals,
                               int64_t p, double* __restrict__ colmax) {
@@ -124,24 +132,21 @@ __global__ void fixed_terms_kernel(const int64_t* __restrict__ col_ptr,
   }
 }
 
-// eta_out[r] = sum_j beta_j x_rj (ascending j within the row, warp tree sum)
+// eta_out[r] = sum_j beta_j x_rj, accumulated in ascending column order
+// exactly as Engine::load_beta does (src/engine.cpp:120-154); thread per row.
 __global__ void spmv_rows_kernel(const int64_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ csr_col,
                                  const double* __restrict__ csr_val,
                                  const uint32_t* __restrict__ code, int64_t n,
                                  const double* __restrict__ beta, double* __restrict__ eta_out,
                                  int* __restrict__ overflow) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < n;
-       r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
     double acc = 0.0;
-    for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32)
+    for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k)
       acc = __dadd_rn(acc, __dmul_rn(beta[csr_col[k]], csr_val ? csr_val[k] : 1.0));
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      eta_out[r] = acc;
-      if (!(code[r] & kCodeMasked) && fabs(acc) > kXbetaBound) *overflow = 1;
-    }
+    eta_out[r] = acc;
+    if (!(code[r] & kCodeMasked) && fabs(acc) > kXbetaBound) *overflow = 1;
   }
 }
 
@@ -163,7 +168,7 @@ __global__ void commit_eta_kernel(const double* __restrict__ eta_in,
     atomicMax(&ctl->eta_absmax_bits, static_cast<unsigned long long>(__double_as_longlong(mx)));
 }
 
-__global__ void update_check_kernel(SweepParams P, int64_t col, double delta, int* overflow) {
+__global__ void update_check_kernel(CycleParams P, int64_t col, double delta, int* overflow) {
   const int64_t k0 = P.col_ptr[col], k1 = P.col_ptr[col + 1];
   const bool ind = !P.has_vals || P.col_ind[col];
   for (int64_t k = k0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < k1;
@@ -175,7 +180,7 @@ __global__ void update_check_kernel(SweepParams P, int64_t col, double delta, in
   }
 }
 
-__global__ void update_commit_kernel(SweepParams P, int64_t col, double delta, double factor) {
+__global__ void update_commit_kernel(CycleParams P, int64_t col, double delta, double factor) {
   const int64_t k0 = P.col_ptr[col], k1 = P.col_ptr[col + 1];
   const bool ind = !P.has_vals || P.col_ind[col];
   double mx = 0.0;
@@ -243,6 +248,13 @@ cudaError_t launch_exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cu
   return e;
 }
 
+cudaError_t launch_remap_rows(int32_t* row_idx, int64_t nnz, const int64_t* dev_row,
+                              cudaStream_t s) {
+  if (nnz == 0) return cudaSuccess;
+  remap_rows_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(row_idx, nnz, dev_row);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s) {
   tile_ptr_kernel<<<grid_for(p * (ntiles + 1), 256), 256, 0, s>>>(col_ptr, row_idx, p, ntiles,
@@ -288,28 +300,28 @@ cudaError_t launch_fixed_terms(const int64_t* col_ptr, const int32_t* row_idx, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv_rows(const SweepParams& prm, const double* beta, double* eta_out,
+cudaError_t launch_spmv_rows(const CycleParams& prm, const double* beta, double* eta_out,
                              int* overflow, cudaStream_t s) {
-  if (prm.n == 0) return cudaSuccess;
-  spmv_rows_kernel<<<grid_for(prm.n * 32, 256), 256, 0, s>>>(
-      prm.row_ptr, prm.csr_col, prm.csr_val, prm.code, prm.n, beta, eta_out, overflow);
+  if (prm.npad == 0) return cudaSuccess;
+  spmv_rows_kernel<<<grid_for(prm.npad, 256), 256, 0, s>>>(
+      prm.row_ptr, prm.csr_col, prm.csr_val, prm.code, prm.npad, beta, eta_out, overflow);
   return cudaGetLastError();
 }
 
-cudaError_t launch_commit_eta(const SweepParams& prm, const double* eta_in, cudaStream_t s) {
-  if (prm.n == 0) return cudaSuccess;
-  commit_eta_kernel<<<grid_for(prm.n, 256), 256, 0, s>>>(eta_in, prm.code, prm.n, prm.eta, prm.e,
+cudaError_t launch_commit_eta(const CycleParams& prm, const double* eta_in, cudaStream_t s) {
+  if (prm.npad == 0) return cudaSuccess;
+  commit_eta_kernel<<<grid_for(prm.npad, 256), 256, 0, s>>>(eta_in, prm.code, prm.npad, prm.eta, prm.e,
                                                          prm.ctl);
   return cudaGetLastError();
 }
 
-cudaError_t launch_update_check(const SweepParams& prm, int64_t col, double delta, int* overflow,
+cudaError_t launch_update_check(const CycleParams& prm, int64_t col, double delta, int* overflow,
                                 cudaStream_t s) {
   update_check_kernel<<<grid_for(1 << 16, 256), 256, 0, s>>>(prm, col, delta, overflow);
   return cudaGetLastError();
 }
 
-cudaError_t launch_update_commit(const SweepParams& prm, int64_t col, double delta, double factor,
+cudaError_t launch_update_commit(const CycleParams& prm, int64_t col, double delta, double factor,
                                  cudaStream_t s) {
   update_commit_kernel<<<grid_for(1 << 16, 256), 256, 0, s>>>(prm, col, delta, factor);
   return cudaGetLastError();

@@ -1,9 +1,15 @@
 // gss_capi.cu — host implementation of the C ABI in include/gss.h.
 //
-// Owns device memory, streams, TMA descriptors and the per-cycle CUDA graph;
-// builds the per-engine row code words and (Fine-Gray) censoring weights on
-// the host, exactly as the reference builds them per Engine
-// (src/engine.cpp:103-118, src/censoring.cpp:39-94).
+// Owns device memory, streams and TMA descriptors; builds the per-engine row
+// code words and (Fine-Gray) censoring weights on the host, exactly as the
+// reference builds them per Engine (src/engine.cpp:103-118,
+// src/censoring.cpp:39-94); drives the persistent cycle kernel
+// (gss_cycle.cu) once per CCD cycle / API evaluation.
+//
+// Device row layout: the reference's sorted order with every stratum padded
+// to a whole number of 2048-row tiles (padding rows are masked: exp(eta) = 0),
+// so no tile spans two strata.  dev_row[i] maps sorted row i to its device
+// position.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -63,17 +69,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D view [rows = npad/kIpt][kIpt] of a row-major per-row array, box = one tile.
+// 2D view [npad*elem/128][128 bytes] of a row-major per-row array; box = one
+// 2048-row tile as 128-byte rows, 128B swizzle.
 int make_tile_map(CUtensorMap* map, void* base, int64_t npad, CUtensorMapDataType dt,
-                  int elem_bytes, CUtensorMapSwizzle sw) {
+                  int elem_bytes) {
   auto fn = encode_fn();
   if (!fn) return fail(GSS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kIpt), static_cast<cuuint64_t>(npad / kIpt)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kIpt) * elem_bytes};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kIpt), static_cast<cuuint32_t>(kThreads)};
+  const int per_row = 128 / elem_bytes;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(per_row), static_cast<cuuint64_t>(npad / per_row)};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(per_row),
+                       static_cast<cuuint32_t>(kTileRows / per_row)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(GSS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return GSS_OK;
@@ -87,13 +97,15 @@ struct gss_dataset {
   int64_t n = 0, p = 0, nnz = 0, npad = 0;
   int ntiles = 0;
   bool has_vals = false;
-  // host copies needed per engine (row codes, IPCW)
+  // host copies needed per engine (row codes, IPCW) — sorted order
   std::vector<double> times;
   std::vector<int32_t> status;
-  std::vector<uint8_t> stratum_start;
+  std::vector<int64_t> stratum_of;   // stratum ordinal per sorted row
+  std::vector<int64_t> dev_row;      // sorted row -> device position
+  std::vector<uint8_t> h_tile_first;
   // device
   int64_t* col_ptr = nullptr;
-  int32_t* row_idx = nullptr;
+  int32_t* row_idx = nullptr;        // device positions
   double* vals = nullptr;
   uint8_t* col_ind = nullptr;
   uint32_t* tile_ptr = nullptr;
@@ -101,6 +113,7 @@ struct gss_dataset {
   int32_t* csr_col = nullptr;
   double* csr_val = nullptr;
   double* colmax = nullptr;
+  uint8_t* tile_first = nullptr;
   int64_t bytes = 0;
   std::vector<int64_t> h_col_ptr;
 
@@ -109,7 +122,8 @@ struct gss_dataset {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     for (void* q : {(void*)col_ptr, (void*)row_idx, (void*)vals, (void*)col_ind, (void*)tile_ptr,
-                    (void*)row_ptr, (void*)csr_col, (void*)csr_val, (void*)colmax})
+                    (void*)row_ptr, (void*)csr_col, (void*)csr_val, (void*)colmax,
+                    (void*)tile_first})
       if (q) cudaFree(q);
     if (prev >= 0) cudaSetDevice(prev);
   }
@@ -122,23 +136,23 @@ struct gss_engine {
   bool weighted = false;
   cudaStream_t stream = nullptr;
   int grid = 1;
-  std::vector<uint32_t> h_code;
-  std::vector<double> h_u, h_g;
+  std::vector<uint32_t> h_code;   // device positions
+  std::vector<double> h_u, h_g;   // sorted order (accessor)
   std::vector<double> h_beta;
+  std::vector<int32_t> h_slots;
   // device
-  double *eta = nullptr, *e = nullptr, *scratch = nullptr, *u = nullptr, *g = nullptr;
+  double *eta = nullptr, *e = nullptr, *scratch = nullptr, *g = nullptr;
   uint32_t* code = nullptr;
   double *beta = nullptr, *halfwidth = nullptr, *fixed = nullptr;
   uint8_t* penalized = nullptr;
-  double *agg = nullptr, *prefix = nullptr, *tsum = nullptr, *gsum = nullptr, *gpre = nullptr;
-  unsigned int* grp_cnt = nullptr;
-  int32_t* tile_lastseg = nullptr;
-  double* tile_part = nullptr;
+  double *trec = nullptr, *tcar = nullptr, *cpay = nullptr, *slot_out = nullptr;
+  int32_t* slot_col = nullptr;
+  unsigned int* bar = nullptr;
   Ctl* ctl = nullptr;
   int* dflag = nullptr;
   Ctl* h_ctl = nullptr;  // pinned mirror
-  CUtensorMap tm_e{}, tm_code{};
-  SweepParams prm{};
+  CUtensorMap tm_e{}, tm_code{}, tm_g{};
+  CycleParams prm{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_launches = 0;
@@ -148,9 +162,9 @@ struct gss_engine {
   ~gss_engine() {
     cudaSetDevice(ds->device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)u, (void*)g, (void*)code,
-                    (void*)beta, (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)agg, (void*)gsum, (void*)gpre, (void*)grp_cnt,
-                    (void*)prefix, (void*)tsum, (void*)tile_lastseg, (void*)tile_part, (void*)ctl,
+    for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
+                    (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
+                    (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
                     (void*)dflag})
       if (q) cudaFree(q);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -195,71 +209,66 @@ int device_error(gss_engine* E, const char* where) {
   // clear for the next call
   E->h_ctl->err_code = 0;
   E->h_ctl->err_col = -1;
-  E->h_ctl->halted = 0;
-  E->h_ctl->pend_col = -1;
-  E->h_ctl->pend_delta = 0.0;
-  E->h_ctl->refresh_pending = 0;
+  E->h_ctl->rec_valid = 0;
   push_ctl(E);
   return fail(code, msg);
 }
 
-// Per-engine row code words over the visible rows (row_mask), stratum by
-// stratum: maximal runs of equal time among visible rows form the tied blocks
-// (src/dataset.cpp:190-204 applied to the subset, src/dataset.cpp:268-322);
-// the run's status==1 count goes to its last visible row.
-void build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t>& code) {
+// Per-engine row code words (device positions) over the visible rows
+// (row_mask), stratum by stratum: maximal runs of equal time among visible
+// rows form the tied blocks (src/dataset.cpp:190-204 applied to the subset,
+// src/dataset.cpp:268-322); the run's status==1 count goes to its last
+// visible row.  Padding rows are masked.
+int build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t>& code) {
   const int64_t n = ds->n;
-  code.assign(static_cast<size_t>(ds->npad), 0u);
-  for (int64_t i = n; i < ds->npad; ++i) code[i] = kCodeMasked;
+  code.assign(static_cast<size_t>(ds->npad), kCodeMasked);
   int64_t s = 0;
   while (s < n) {
     int64_t e = s + 1;
-    if (!ds->stratum_start.empty())
-      while (e < n && !ds->stratum_start[e]) ++e;
-    else
-      e = n;
-    code[s] |= kCodeSeg;
+    while (e < n && ds->stratum_of[e] == ds->stratum_of[s]) ++e;
     int64_t last_vis = -1;
     double last_t = 0.0;
     uint32_t cnt = 0;
     for (int64_t i = s; i < e; ++i) {
+      uint32_t& c = code[ds->dev_row[i]];
+      c = (i == s) ? kCodeSeg : 0u;
       const bool vis = !mask || mask[i];
       if (!vis) {
-        code[i] |= kCodeMasked;
+        c |= kCodeMasked;
         continue;
       }
       if (last_vis >= 0 && ds->times[i] != last_t) {
-        code[last_vis] |= cnt;
+        code[ds->dev_row[last_vis]] |= cnt;
         cnt = 0;
       }
       if (ds->status[i] == 1) {
-        ++cnt;
-        code[i] |= kCodeEvent;
+        if (++cnt > kCodeCount) return fail(GSS_ERR_DOMAIN, "tied block exceeds 2^28 events");
+        c |= kCodeEvent;
+      } else if (ds->status[i] == 2) {
+        c |= kCodeCompeting;
       }
       last_vis = i;
       last_t = ds->times[i];
     }
-    if (last_vis >= 0) code[last_vis] |= cnt;
+    if (last_vis >= 0) code[ds->dev_row[last_vis]] |= cnt;
     s = e;
   }
+  return GSS_OK;
 }
 
 // Kaplan-Meier of the censoring distribution over the visible rows of each
 // stratum, failures before censorings on ties, then u = 1/G(Y-) on competing
-// rows and g = G(Y-) (src/censoring.cpp:39-90).
+// rows and g = G(Y-) (src/censoring.cpp:39-90).  Sorted order.
 int build_ipcw_host(const gss_dataset* ds, const uint8_t* mask, std::vector<double>& u,
                     std::vector<double>& g) {
   const int64_t n = ds->n;
-  u.assign(static_cast<size_t>(ds->npad), 0.0);
-  g.assign(static_cast<size_t>(ds->npad), 1.0);
+  u.assign(static_cast<size_t>(n), 0.0);
+  g.assign(static_cast<size_t>(n), 1.0);
   std::vector<int64_t> rows, ends;
   int64_t s = 0;
   while (s < n) {
     int64_t e = s + 1;
-    if (!ds->stratum_start.empty())
-      while (e < n && !ds->stratum_start[e]) ++e;
-    else
-      e = n;
+    while (e < n && ds->stratum_of[e] == ds->stratum_of[s]) ++e;
     rows.clear();
     for (int64_t i = s; i < e; ++i)
       if (!mask || mask[i]) rows.push_back(i);
@@ -304,9 +313,19 @@ int check_engine(gss_engine* E) {
   return GSS_OK;
 }
 
-int launch(gss_engine* E, int mode, int64_t column) {
-  E->prm.column = column;
-  GSS_CUDA(launch_sweep(mode, &E->tm_e, &E->tm_code, E->prm, E->grid, E->stream));
+// One launch of the cycle kernel over `slots` (API or CCD mode).
+int run_slots(gss_engine* E, const std::vector<int32_t>& slots, int mode, bool want_out) {
+  if (slots.empty()) return GSS_OK;
+  if (static_cast<int64_t>(slots.size()) > E->ds->p + 1)
+    return fail(GSS_ERR_DOMAIN, "too many slots");
+  GSS_CUDA(cudaMemcpyAsync(E->slot_col, slots.data(), slots.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice, E->stream));
+  CycleParams P = E->prm;
+  P.slot_col = E->slot_col;
+  P.nslots = static_cast<int>(slots.size());
+  P.mode = mode;
+  P.slot_out = want_out ? E->slot_out : nullptr;
+  GSS_CUDA(launch_cycle(&E->tm_e, &E->tm_code, &E->tm_g, P, E->stream));
   return GSS_OK;
 }
 
@@ -330,7 +349,7 @@ extern "C" {
 const char* gss_last_error(void) { return g_last_error.c_str(); }
 
 const char* gss_version(void) {
-  return "gss 0.1.0 (sm_100a; tile=2048 rows; decoupled look-back fp64 scan)";
+  return "gss 0.2.0 (sm_100a; persistent cycle kernel; tile=2048 rows; fp64)";
 }
 
 int gss_device_count(void) {
@@ -343,8 +362,6 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   if (!h || !out) return fail(GSS_ERR_DOMAIN, "null argument");
   *out = nullptr;
   if (h->n < 0 || h->p < 0) return fail(GSS_ERR_DOMAIN, "negative dimensions");
-  if (h->n >= (int64_t(1) << 31) - kTileRows)
-    return fail(GSS_ERR_DOMAIN, "dataset too large for 32-bit row offsets");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(GSS_ERR_NO_DEVICE, "no CUDA device available");
@@ -367,12 +384,39 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   ds->n = n;
   ds->p = p;
   ds->nnz = nnz;
-  ds->ntiles = static_cast<int>((n + kTileRows - 1) / kTileRows);
-  if (ds->ntiles == 0) ds->ntiles = 1;
-  ds->npad = int64_t(ds->ntiles) * kTileRows;
   ds->times.assign(h->times, h->times + n);
   ds->status.assign(h->status, h->status + n);
-  if (h->stratum_start) ds->stratum_start.assign(h->stratum_start, h->stratum_start + n);
+  // stratum-aligned device layout
+  ds->stratum_of.resize(static_cast<size_t>(n));
+  ds->dev_row.resize(static_cast<size_t>(n));
+  {
+    int64_t stratum = -1, pos = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (i == 0 || (h->stratum_start && h->stratum_start[i])) {
+        ++stratum;
+        pos = (pos + kTileRows - 1) / kTileRows * kTileRows;  // next tile boundary
+      }
+      ds->stratum_of[i] = stratum;
+      ds->dev_row[i] = pos++;
+    }
+    int64_t npad = (pos + kTileRows - 1) / kTileRows * kTileRows;
+    if (npad == 0) npad = kTileRows;
+    if (npad >= (int64_t(1) << 31) - kTileRows) {
+      delete ds;
+      return fail(GSS_ERR_DOMAIN, "dataset too large for 32-bit row positions");
+    }
+    if (npad > 4 * n + 64 * int64_t(kTileRows)) {
+      delete ds;
+      return fail(GSS_ERR_DOMAIN, "too many small strata for the tile-aligned device layout");
+    }
+    ds->npad = npad;
+    ds->ntiles = static_cast<int>(npad / kTileRows);
+    ds->h_tile_first.assign(static_cast<size_t>(ds->ntiles), 0);
+    ds->h_tile_first[0] = 1;
+    for (int64_t i = 0; i < n; ++i)
+      if (i == 0 || ds->stratum_of[i] != ds->stratum_of[i - 1])
+        ds->h_tile_first[ds->dev_row[i] / kTileRows] = 1;
+  }
   ds->h_col_ptr.assign(h->col_ptr, h->col_ptr + p + 1);
   if (p == 0) ds->h_col_ptr.assign(1, 0);
   // indicator flags: given, or all-ones & density < 25% (src/dataset.cpp:126-157)
@@ -405,19 +449,21 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
       return cleanup(fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA, \
                           std::string("CUDA error in pack: ") + cudaGetErrorString(_e))); \
   } while (0)
+  const int64_t npad = ds->npad;
   PK(dalloc(&ds->col_ptr, p + 1));
   PK(dalloc(&ds->row_idx, nnz + 4));
   PK(dalloc(&ds->col_ind, p));
   PK(dalloc(&ds->tile_ptr, p * (ds->ntiles + 1)));
-  PK(dalloc(&ds->row_ptr, n + 1));
+  PK(dalloc(&ds->row_ptr, npad + 1));
   PK(dalloc(&ds->csr_col, nnz + 4));
   PK(dalloc(&ds->colmax, p));
+  PK(dalloc(&ds->tile_first, ds->ntiles));
   if (ds->has_vals) {
     PK(dalloc(&ds->vals, nnz + 4));
     PK(dalloc(&ds->csr_val, nnz + 4));
   }
-  ds->bytes = (p + 1) * 8 + (nnz + 4) * 8 + p + int64_t(p) * (ds->ntiles + 1) * 4 + (n + 1) * 8 +
-              p * 8 + (ds->has_vals ? (nnz + 4) * 16 : 0);
+  ds->bytes = (p + 1) * 8 + (nnz + 4) * 8 + p + int64_t(p) * (ds->ntiles + 1) * 4 +
+              (npad + 1) * 8 + p * 8 + ds->ntiles + (ds->has_vals ? (nnz + 4) * 16 : 0);
   PK(cudaMemcpyAsync(ds->col_ptr, ds->h_col_ptr.data(), (p + 1) * sizeof(int64_t),
                      cudaMemcpyHostToDevice, s));
   PK(cudaMemsetAsync(ds->row_idx, 0, (nnz + 4) * sizeof(int32_t), s));
@@ -426,6 +472,8 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   if (p) PK(cudaMemcpyAsync(ds->col_ind, ind.data(), p, cudaMemcpyHostToDevice, s));
   if (ds->has_vals && nnz)
     PK(cudaMemcpyAsync(ds->vals, h->vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  PK(cudaMemcpyAsync(ds->tile_first, ds->h_tile_first.data(), ds->ntiles, cudaMemcpyHostToDevice,
+                     s));
   {
     int* bad = nullptr;
     PK(dalloc(&bad, 1));
@@ -439,21 +487,30 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     if (hb) return cleanup(fail(GSS_ERR_DOMAIN, "CSC columns must have monotone col_ptr and "
                                                 "strictly ascending row indices"));
   }
+  if (npad != n) {  // remap to the stratum-aligned positions (order preserving)
+    int64_t* drow = nullptr;
+    PK(dalloc(&drow, std::max<int64_t>(n, 1)));
+    if (n)
+      PK(cudaMemcpyAsync(drow, ds->dev_row.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    PK(launch_remap_rows(ds->row_idx, nnz, drow, s));
+    PK(cudaStreamSynchronize(s));
+    cudaFree(drow);
+  }
   if (p) {
     PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
     PK(launch_colmax(ds->col_ptr, ds->has_vals ? ds->vals : nullptr, p, ds->colmax, s));
   }
-  // CSR transpose: count -> host exclusive scan -> fill -> per-row sort
+  // CSR transpose over device positions: count -> exclusive scan -> fill -> per-row sort
   {
     int64_t* cnt = nullptr;
-    PK(dalloc(&cnt, n + 1));
-    PK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int64_t), s));
+    PK(dalloc(&cnt, npad + 1));
+    PK(cudaMemsetAsync(cnt, 0, (npad + 1) * sizeof(int64_t), s));
     PK(launch_csr_count(ds->row_idx, nnz, cnt, s));
-    PK(launch_exclusive_scan(cnt, ds->row_ptr, n + 1, s));
-    PK(cudaMemcpyAsync(cnt, ds->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    PK(launch_exclusive_scan(cnt, ds->row_ptr, npad + 1, s));
+    PK(cudaMemcpyAsync(cnt, ds->row_ptr, (npad + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     PK(launch_csr_fill(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, p, cnt,
                        ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
-    PK(launch_csr_sort_rows(ds->row_ptr, n, ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
+    PK(launch_csr_sort_rows(ds->row_ptr, npad, ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
     PK(cudaStreamSynchronize(s));
     cudaFree(cnt);
   }
@@ -487,14 +544,22 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   E->model = model;
   E->interval = recompute_interval;
   E->weighted = model == GSS_FINE_GRAY && competing;  // src/engine.cpp:237
-  if (E->weighted) {
-    delete E;
-    return fail(GSS_ERR_DOMAIN,
-                "fine_gray with competing rows is not yet available on the device path");
+  {
+    int rc = build_codes(ds, row_mask, E->h_code);
+    if (rc) {
+      delete E;
+      return rc;
+    }
   }
-  build_codes(ds, row_mask, E->h_code);
+  if (E->weighted) {
+    int rc = build_ipcw_host(ds, row_mask, E->h_u, E->h_g);
+    if (rc) {
+      delete E;
+      return rc;
+    }
+  }
   const int64_t n = ds->n, p = ds->p, npad = ds->npad;
-  const int nt = ds->ntiles, ng = nt / kGroup + 1;
+  const int nt = ds->ntiles;
   auto bail = [&](int rc) {
     delete E;
     return rc;
@@ -506,6 +571,9 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
       return bail(fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA,    \
                        std::string("CUDA error in engine_create: ") + cudaGetErrorString(_e))); \
   } while (0)
+  int maxg = cycle_max_grid(ds->device, E->weighted);
+  if (maxg < 1) return bail(fail(GSS_ERR_CUDA, "cycle kernel cannot be resident on this device"));
+  E->grid = std::max(1, std::min(nt, maxg));
   EK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
   EK(cudaEventCreate(&E->ev0));
   EK(cudaEventCreate(&E->ev1));
@@ -517,57 +585,55 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(dalloc(&E->halfwidth, p));
   EK(dalloc(&E->fixed, p));
   EK(dalloc(&E->penalized, p));
-  EK(dalloc(&E->agg, size_t(nt) * 4));
-  EK(dalloc(&E->prefix, size_t(nt) * 4));
-  EK(dalloc(&E->tsum, size_t(nt) * 4));
-  EK(dalloc(&E->gsum, size_t(nt / 32 + 1) * 4));
-  EK(dalloc(&E->gpre, size_t(nt / 32 + 1) * 4));
-  EK(dalloc(&E->grp_cnt, size_t(nt / 32 + 1)));
-  EK(cudaMemsetAsync(E->grp_cnt, 0, size_t(nt / 32 + 1) * sizeof(unsigned), E->stream));
-  EK(dalloc(&E->tile_lastseg, nt));
-  EK(dalloc(&E->tile_part, size_t(nt) * 4));
+  EK(dalloc(&E->trec, size_t(nt) * kRecStride));
+  EK(dalloc(&E->tcar, size_t(nt) * kCarStride));
+  EK(dalloc(&E->cpay, size_t(2) * E->grid * kPayStride));
+  EK(dalloc(&E->slot_out, size_t(p + 1) * 4));
+  EK(dalloc(&E->slot_col, size_t(p + 1)));
+  EK(dalloc(&E->bar, 1));
   EK(dalloc(&E->ctl, 1));
   EK(dalloc(&E->dflag, 4));
+  if (E->weighted) EK(dalloc(&E->g, npad));
   EK(cudaMallocHost(reinterpret_cast<void**>(&E->h_ctl), sizeof(Ctl)));
   std::memset(E->h_ctl, 0, sizeof(Ctl));
-  E->h_ctl->epoch = 1;
-  E->h_ctl->pend_col = -1;
   E->h_ctl->err_col = -1;
+  E->h_ctl->rec_col = -2;
   cudaStream_t s = E->stream;
+  EK(cudaMemsetAsync(E->bar, 0, sizeof(unsigned), s));
+  EK(cudaMemsetAsync(E->trec, 0, size_t(nt) * kRecStride * sizeof(double), s));
+  EK(cudaMemsetAsync(E->tcar, 0, size_t(nt) * kCarStride * sizeof(double), s));
   EK(cudaMemcpyAsync(E->code, E->h_code.data(), npad * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   EK(cudaMemsetAsync(E->eta, 0, npad * sizeof(double), s));
   {
     std::vector<double> e0(static_cast<size_t>(npad), 0.0);
-    for (int64_t i = 0; i < n; ++i) e0[i] = (E->h_code[i] & kCodeMasked) ? 0.0 : 1.0;
+    for (int64_t i = 0; i < npad; ++i) e0[i] = (E->h_code[i] & kCodeMasked) ? 0.0 : 1.0;
     EK(cudaMemcpyAsync(E->e, e0.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
-    EK(cudaStreamSynchronize(s));
+    if (E->weighted) {
+      std::vector<double> gd(static_cast<size_t>(npad), 1.0);
+      for (int64_t i = 0; i < n; ++i) gd[ds->dev_row[i]] = E->h_g[i];
+      EK(cudaMemcpyAsync(E->g, gd.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
+      EK(cudaStreamSynchronize(s));
+    } else {
+      EK(cudaStreamSynchronize(s));
+    }
   }
   EK(cudaMemsetAsync(E->beta, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
-
-  {
-    std::vector<int32_t> ls(static_cast<size_t>(nt), -1);
-    for (int64_t i = 0; i < npad; ++i)
-      if (E->h_code[i] & kCodeSeg) ls[i / kTileRows] = static_cast<int32_t>(i % kTileRows);
-    EK(cudaMemcpyAsync(E->tile_lastseg, ls.data(), nt * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    EK(cudaStreamSynchronize(s));
-  }
   EK(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   EK(launch_fixed_terms(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, ds->col_ind,
                         E->code, p, E->fixed, s));
   EK(cudaStreamSynchronize(s));
   E->h_beta.assign(static_cast<size_t>(p), 0.0);
-  int rc = make_tile_map(&E->tm_e, E->e, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8,
-                         CU_TENSOR_MAP_SWIZZLE_64B);
+  int rc = make_tile_map(&E->tm_e, E->e, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8);
   if (rc) return bail(rc);
-  rc = make_tile_map(&E->tm_code, E->code, npad, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4,
-                     CU_TENSOR_MAP_SWIZZLE_32B);
+  rc = make_tile_map(&E->tm_code, E->code, npad, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4);
   if (rc) return bail(rc);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ds->device);
-  int occ = sweep_max_active_ctas_per_sm();
-  if (occ < 1) occ = 1;
-  E->grid = std::max(1, std::min(nt, sms * occ));
-  SweepParams& P = E->prm;
+  if (E->weighted) {
+    rc = make_tile_map(&E->tm_g, E->g, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8);
+    if (rc) return bail(rc);
+  } else {
+    E->tm_g = E->tm_e;
+  }
+  CycleParams& P = E->prm;
   P.n = n;
   P.npad = npad;
   P.p = p;
@@ -582,39 +648,31 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.csr_col = ds->csr_col;
   P.csr_val = ds->csr_val;
   P.colmax = ds->colmax;
+  P.tile_first = ds->tile_first;
   P.eta = E->eta;
   P.e = E->e;
   P.code = E->code;
-  P.u = E->u;
   P.g = E->g;
   P.beta = E->beta;
   P.halfwidth = E->halfwidth;
   P.penalized = E->penalized;
   P.fixed = E->fixed;
-  P.pen_kind = 0;
   P.weighted = E->weighted ? 1 : 0;
+  P.pen_kind = 0;
   P.pen_strength = 0.0;
   P.recompute_interval = recompute_interval;
-  P.agg = E->agg;
-  P.prefix = E->prefix;
-  P.tsum = E->tsum;
-  P.gsum = E->gsum;
-  P.gpre = E->gpre;
-  P.grp_cnt = E->grp_cnt;
-  P.has_mask = row_mask ? 1 : 0;
-  P.has_strata = 0;
-  for (int64_t i = 1; i < n; ++i)
-    if (E->h_code[i] & kCodeSeg) P.has_strata = 1;
-  P.tile_lastseg = E->tile_lastseg;
-  P.tile_part = E->tile_part;
+  P.grid = E->grid;
+  P.trec = E->trec;
+  P.tcar = E->tcar;
+  P.cpay = E->cpay;
+  P.bar = E->bar;
   P.ctl = E->ctl;
-  P.column = 0;
+  if (const char* dbg = std::getenv("GSS_DEBUG")) P.dbg = std::atoi(dbg);
   if (const char* tr = std::getenv("GSS_TRACE")) {
     if (tr[0] == '1') {
-      P.trace_cap = 1u << 22;
+      P.trace_cap = 32u << 16;  // 32 warps x 65536 events (CTA 0)
       EK(dalloc(&P.trace, size_t(P.trace_cap) * 2));
-      EK(dalloc(&P.trace_n, 1));
-      EK(cudaMemset(P.trace_n, 0, sizeof(unsigned)));
+      EK(cudaMemset(P.trace, 0, size_t(P.trace_cap) * 16));
     }
   }
 #undef EK
@@ -632,7 +690,6 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
                                             " coefficients, got " + std::to_string(p));
   for (int64_t j = 0; j < p; ++j)
     if (!std::isfinite(beta[j])) return fail(GSS_ERR_DOMAIN, "load_beta: non-finite coefficient");
-  // scratch beta lives in the tail of `scratch`? keep a dedicated upload buffer
   double* dbeta = nullptr;
   GSS_CUDA(dalloc(&dbeta, p));
   cudaStream_t s = E->stream;
@@ -654,16 +711,15 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
     return fail(GSS_ERR_OVERFLOW, "load_beta: |x'beta| exceeds 700");
   }
   if (p) GSS_CUDA(cudaMemcpyAsync(E->beta, dbeta, p * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  E->h_ctl->tprev_valid = 0;      // e rewritten outside a sweep: per-tile sums stale
+  E->h_ctl->rec_valid = 0;        // e rewritten outside the cycle kernel
   E->h_ctl->eta_absmax_bits = 0;  // fresh eta: the bound is rebuilt exactly by the commit
-  E->h_ctl->absmax_next_bits = 0;
   E->h_ctl->bound_slack = 0.0;
   GSS_CUDA(cudaMemcpyAsync(E->ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   GSS_CUDA(launch_commit_eta(E->prm, E->scratch, s));
   GSS_CUDA(cudaStreamSynchronize(s));
   cudaFree(dbeta);
   E->h_beta.assign(beta, beta + p);
-  return GSS_OK;
+  return sync_ctl(E);
 }
 
 int gss_engine_refresh(gss_engine* E) {
@@ -700,7 +756,7 @@ int gss_engine_update(gss_engine* E, int64_t column, double delta) {
   rc = sync_ctl(E);
   if (rc) return rc;
   E->h_ctl->accepted += 1;
-  E->h_ctl->tprev_valid = 0;  // e changed outside a sweep
+  E->h_ctl->rec_valid = 0;  // e changed outside the cycle kernel
   const bool refresh = E->h_ctl->accepted % E->interval == 0;
   rc = push_ctl(E);
   if (rc) return rc;
@@ -715,7 +771,7 @@ int gss_engine_grad_hessian(gss_engine* E, int64_t column, double* gradient, dou
   if (column < 0 || column >= E->ds->p)
     return fail(GSS_ERR_INVALID_COLUMN, "grad_hessian: column " + std::to_string(column) +
                                             " outside [0, " + std::to_string(E->ds->p) + ")");
-  rc = launch(E, kModeGradApi, column);
+  rc = run_slots(E, {static_cast<int32_t>(column)}, kModeApi, false);
   if (rc) return rc;
   rc = sync_ctl(E);
   if (rc) return rc;
@@ -729,7 +785,7 @@ int gss_engine_grad_hessian(gss_engine* E, int64_t column, double* gradient, dou
 int gss_engine_log_likelihood(gss_engine* E, double* out) {
   int rc = check_engine(E);
   if (rc) return rc;
-  rc = launch(E, kModeLoglik, 0);
+  rc = run_slots(E, {-1}, kModeApi, false);
   if (rc) return rc;
   rc = sync_ctl(E);
   if (rc) return rc;
@@ -750,8 +806,11 @@ static int get_rows(gss_engine* E, const double* src, double* out, int64_t n) {
   int rc = check_engine(E);
   if (rc) return rc;
   if (n != E->ds->n) return fail(GSS_ERR_DOMAIN, "row array size mismatch");
-  if (n) GSS_CUDA(cudaMemcpyAsync(out, src, n * sizeof(double), cudaMemcpyDeviceToHost, E->stream));
+  std::vector<double> tmp(static_cast<size_t>(E->ds->npad));
+  GSS_CUDA(cudaMemcpyAsync(tmp.data(), src, E->ds->npad * sizeof(double), cudaMemcpyDeviceToHost,
+                           E->stream));
   GSS_CUDA(cudaStreamSynchronize(E->stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = tmp[E->ds->dev_row[i]];
   return GSS_OK;
 }
 
@@ -798,11 +857,11 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t p = E->ds->p;
   // PenaltySpec::validate / FitConfig::validate (src/ccd.cpp:37-69)
+  if (pen->kind < 0 || pen->kind > 2) return fail(GSS_ERR_DOMAIN, "unknown penalty");
   if (pen->kind == GSS_PEN_L1 && (!std::isfinite(pen->strength) || pen->strength < 0.0))
     return fail(GSS_ERR_DOMAIN, "l1 strength must be finite and >= 0");
   if (pen->kind == GSS_PEN_L2 && (!std::isfinite(pen->strength) || pen->strength <= 0.0))
     return fail(GSS_ERR_DOMAIN, "l2 strength must be finite and > 0");
-  if (pen->kind < 0 || pen->kind > 2) return fail(GSS_ERR_DOMAIN, "unknown penalty");
   if (!std::isfinite(cfg->tolerance) || cfg->tolerance <= 0.0)
     return fail(GSS_ERR_DOMAIN, "tolerance must be > 0");
   if (cfg->max_cycles < 1) return fail(GSS_ERR_DOMAIN, "max_cycles must be >= 1");
@@ -828,11 +887,8 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   rc = sync_ctl(E);
   if (rc) return rc;
   E->h_ctl->skipped = 0;
-  E->h_ctl->pend_col = -1;
-  E->h_ctl->pend_delta = 0.0;
-  E->h_ctl->refresh_pending = 0;
-  E->h_ctl->halted = 0;
   E->h_ctl->err_code = 0;
+  E->h_ctl->err_col = -1;
   rc = push_ctl(E);
   if (rc) return rc;
 
@@ -844,25 +900,10 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   if (trace_out) trace_out[0] = prev;
   bool converged = p == 0;
 
-  // capture one cycle: p fused coordinate sweeps + the objective sweep
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  if (!converged) {
-    GSS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int64_t j = 0; j < p; ++j) {
-      E->prm.column = j;
-      cudaError_t le = launch_sweep(kModeGradCcd, &E->tm_e, &E->tm_code, E->prm, E->grid, s);
-      if (le != cudaSuccess) {
-        cudaStreamEndCapture(s, &graph);
-        if (graph) cudaGraphDestroy(graph);
-        return fail(GSS_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(le));
-      }
-    }
-    E->prm.column = 0;
-    GSS_CUDA(launch_sweep(kModeLoglik, &E->tm_e, &E->tm_code, E->prm, E->grid, s));
-    GSS_CUDA(cudaStreamEndCapture(s, &graph));
-    GSS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  }
+  // one cycle = p coordinate slots + the objective slot, one kernel launch
+  std::vector<int32_t> slots(static_cast<size_t>(p + 1));
+  for (int64_t j = 0; j < p; ++j) slots[j] = static_cast<int32_t>(j);
+  slots[p] = -1;
   double dev_ms = 0.0;
   E->cycle_ms.clear();
   E->cycle_accepted.clear();
@@ -870,12 +911,9 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   int err = GSS_OK;
   for (cycle = 1; !converged && cycle <= cfg->max_cycles; ++cycle) {
     cudaEventRecord(E->ev0, s);
-    cudaError_t le = cudaGraphLaunch(exec, s);
+    err = run_slots(E, slots, kModeCcd, false);
     cudaEventRecord(E->ev1, s);
-    if (le != cudaSuccess) {
-      err = fail(GSS_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(le));
-      break;
-    }
+    if (err) break;
     err = sync_ctl(E);
     if (err) break;
     float ms = 0.f;
@@ -883,24 +921,20 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
     dev_ms += ms;
     E->cycle_ms.push_back(ms);
     E->cycle_accepted.push_back(E->h_ctl->accepted);
+    if (p) cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
     if (E->h_ctl->err_code) {
-      // keep the device beta (already-accepted updates) visible to the caller
-      cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
       err = device_error(E, "fit");
       break;
     }
     res->cycles = cycle;
-    if (p) cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
     const double obj = E->h_ctl->loglik - penalty_value(pen, E->h_beta);
     if (trace_out) trace_out[cycle] = obj;
     if (obj < prev - 1e-10) ++res->monotonicity_violations;
     if (std::abs(obj - prev) / std::max(1.0, std::abs(obj)) < cfg->tolerance) converged = true;
     prev = obj;
   }
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
   E->last_ms = dev_ms;
-  E->last_launches = res->cycles * (p + 1);
+  E->last_launches = res->cycles;
   if (err) return err;
   res->converged = converged ? 1 : 0;
   res->objective = prev;
@@ -914,16 +948,37 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   return GSS_OK;
 }
 
-int gss_engine_max_abs_gradient(gss_engine* E, double* out) {
+int gss_engine_grad_hessian_all(gss_engine* E, double* gradient, double* hessian,
+                                double* fixed_term) {
   int rc = check_engine(E);
   if (rc) return rc;
-  double top = 0.0;
-  for (int64_t j = 0; j < E->ds->p; ++j) {
-    double g = 0.0;
-    rc = gss_engine_grad_hessian(E, j, &g, nullptr, nullptr);
-    if (rc) return rc;
-    top = std::max(top, std::abs(g));
+  const int64_t p = E->ds->p;
+  if (p == 0) return GSS_OK;
+  std::vector<int32_t> slots(static_cast<size_t>(p));
+  for (int64_t j = 0; j < p; ++j) slots[j] = static_cast<int32_t>(j);
+  rc = run_slots(E, slots, kModeApi, true);
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (E->h_ctl->err_code) return device_error(E, "grad_hessian");
+  std::vector<double> outv(static_cast<size_t>(p) * 4);
+  GSS_CUDA(cudaMemcpy(outv.data(), E->slot_out, outv.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+  for (int64_t j = 0; j < p; ++j) {
+    if (gradient) gradient[j] = outv[j * 4];
+    if (hessian) hessian[j] = outv[j * 4 + 1];
+    if (fixed_term) fixed_term[j] = outv[j * 4 + 2];
   }
+  return GSS_OK;
+}
+
+int gss_engine_max_abs_gradient(gss_engine* E, double* out) {
+  const int64_t p = E ? E->ds->p : 0;
+  std::vector<double> g(static_cast<size_t>(p));
+  int rc = gss_engine_grad_hessian_all(E, g.data(), nullptr, nullptr);
+  if (rc) return rc;
+  double top = 0.0;
+  for (double v : g) top = std::max(top, std::abs(v));
   *out = top;
   return GSS_OK;
 }
@@ -935,14 +990,14 @@ int gss_engine_last_timing(gss_engine* E, double* scan_ms, int64_t* launches) {
   return GSS_OK;
 }
 
-// Debug: copy the event trace (GSS_TRACE=1) to host; returns events copied.
+// Debug: copy the event trace (GSS_TRACE=1) to host and reset it; returns events copied.
+// Debug: copy the CTA-0 event trace (trace build + GSS_TRACE=1) and clear it.
+// Layout [32 warps][65536][2] (timestamp 0 = unused); returns the entries copied.
 int64_t gss_engine_trace(gss_engine* E, unsigned long long* out, int64_t max_events) {
   if (!E || !E->prm.trace) return 0;
-  unsigned n = 0;
-  cudaMemcpy(&n, E->prm.trace_n, sizeof(unsigned), cudaMemcpyDeviceToHost);
-  const int64_t k = std::min<int64_t>(std::min<int64_t>(n, E->prm.trace_cap), max_events);
-  cudaMemcpy(out, E->prm.trace, size_t(k) * 16, cudaMemcpyDeviceToHost);
-  cudaMemset(E->prm.trace_n, 0, sizeof(unsigned));
+  const int64_t k = std::min<int64_t>(E->prm.trace_cap, max_events);
+  if (out && k) cudaMemcpy(out, E->prm.trace, size_t(k) * 16, cudaMemcpyDeviceToHost);
+  cudaMemset(E->prm.trace, 0, size_t(E->prm.trace_cap) * 16);
   return k;
 }
 

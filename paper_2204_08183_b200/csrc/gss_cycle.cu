@@ -1,0 +1,1743 @@
+// gss_cycle.cu — the sm_100a CCD hot path: ONE persistent kernel per call
+// that walks a list of "slots" (coordinates of a CCD cycle, or a
+// log-likelihood evaluation) over the time-ordered rows.
+//
+// Per slot it computes what the reference computes per coordinate
+//   * the fused reverse-time risk-set scan -> Breslow transform -> reduce of
+//     detail::fused_grad_hess (/root/reference/proj/include/survscan/scan_kernels.hpp:74-214),
+//     Cox (3 lanes) or Fine-Gray (3 forward + 3 u-weighted backward lanes),
+//     plus Engine::finish (src/engine.cpp:220-230);
+//   * or the log-likelihood of Engine::log_likelihood (src/engine.cpp:331-341,
+//     src/scan.cpp:233-250, 275-367);
+//   * in CCD mode, coordinate_step (src/ccd.cpp:71-129) and the sparse
+//     eta/exp(eta) update of Engine::update_xbeta_sparse (src/engine.cpp:162-218),
+//     with the periodic refresh (src/engine.cpp:120-160).
+//
+// Layout.  Rows live in 2048-row tiles (strata padded so a tile never spans
+// two strata).  CTA c owns a fixed contiguous tile range.  Per CTA:
+//   producer warp : streams (slot, tile) positions through an S-stage smem ring
+//                   — exp(eta) and row codes (and Fine-Gray G(Y-)) as 2D TMA
+//                   boxes, plus the tile's slice of three CSC index lists
+//                   (pending-update column, scan column, next column) as 1D
+//                   bulk copies.  It runs ahead across slot boundaries.
+//   consumer warps: one warp per tile: patch the pending update into the
+//                   staged tile and commit it, 8 passes of (thread-serial 8
+//                   rows -> warp scan), transform at tied-block ends, and the
+//                   next slot's per-tile record (lane sums needed by the carry).
+// Carry.  A tile's risk-set carry is the sum of all earlier rows.  It is
+// assembled from per-tile records written by the previous slot's consumers;
+// the exp(delta) change of the pending indicator update enters linearly
+// ((phi-1) * s-part), so ONE grid-wide exchange per slot suffices: each CTA
+// publishes its partial sums + range aggregates, every CTA reduces them in a
+// fixed order and computes the identical coordinate step, then the carries.
+// Valued pending columns and refreshes take an extra exchange.
+// Determinism: every sum has a fixed order independent of scheduling, so
+// results are bitwise reproducible run to run (scan_kernels.hpp:8-10).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gss_device.cuh"
+#include "gss_kernels.cuh"
+
+namespace gss {
+
+namespace {
+
+constexpr double kXbetaBound = 700.0;  // src/engine.cpp:12
+constexpr double kHwFloor = 1e-300;    // src/ccd.cpp:13
+constexpr double kFastBound = 700.0 * (1.0 - 1e-12);
+constexpr int kErrNonPos = 7;     // GSS_ERR_NONPOS_DEN (include/gss.h)
+constexpr int kErrOverflow = 8;   // GSS_ERR_OVERFLOW
+
+template <bool FG>
+struct Geo {
+  static constexpr int kW = 16;           // consumer warps
+  static constexpr int kGW = FG ? 8 : 4;  // warps per tile group (kPasses / kGW passes each)
+  static_assert(kPasses % kGW == 0 && kW % kGW == 0, "group geometry");
+  static constexpr int kNG = kW / kGW;    // tile groups (tiles in process at once)
+  static constexpr int kS = FG ? 4 : 7;   // ring stages
+  static constexpr uint32_t kEBytes = kTileRows * 8;
+  static constexpr uint32_t kCBytes = kTileRows * 4;
+  static constexpr uint32_t kGBytes = FG ? kTileRows * 8 : 0;
+  static constexpr uint32_t kLBytes = kNnzCap * 4;
+  static constexpr uint32_t kOffC = kEBytes;
+  static constexpr uint32_t kOffG = kEBytes + kCBytes;
+  static constexpr uint32_t kOffL = kEBytes + kCBytes + kGBytes;
+  static constexpr uint32_t kStage = kOffL + 3 * kLBytes;
+  static constexpr int kThreads = 32 * (kW + 1);
+  static_assert(kStage % 1024 == 0, "stage alignment");
+};
+
+struct ListRef {
+  long long lo;   // global index of the first entry of the tile's slice
+  int cnt;        // entries
+  int off;        // smem index of entry 0 (lo - aligned base), -1 => read global
+};
+
+struct StageInfo {
+  int tile, slot;
+  ListRef l[3];  // 0 pending column, 1 scan column, 2 next column
+};
+
+struct SlotState {
+  long long col;   // scan column of the slot (-1: log-likelihood slot)
+  long long pcol;  // pending-update column (-1: none)
+  double delta, phi;
+  int pind;        // pending column is an indicator column
+  int cind;        // scan column is an indicator column
+  int nind;        // next column is an indicator column
+  int refresh;     // staged exp(eta) is stale (a refresh ran): reload from global
+  int fused;       // Cox CCD slot with indicator scan + next columns: fused records
+  int dry;         // halted: stream without work
+  int kind;
+  double cin_f[6];   // corrected fwd carry into the CTA range (a,b,c) + spare
+  double cin_r[6];   // corrected rev carry into the CTA range (ua,ub,uc)
+};
+
+template <bool FG>
+struct Tail {
+  static constexpr int W = Geo<FG>::kW, S = Geo<FG>::kS;
+  uint64_t full[S];
+  uint64_t empty[S];
+  StageInfo info[S];
+  static constexpr int NG = Geo<FG>::kNG, GW = Geo<FG>::kGW;
+  uint32_t xm[NG][2][256];  // per-group scan-column bitmask per thread-row (+ first-entry
+                            // offset), double-buffered by the group's tile parity
+  uint32_t xn[NG][2][256];  // per-group next-column bitmask (fused records)
+  double gx[NG][GW][8];  // per-warp pass-group totals (group exchange)
+  double gr[NG][GW][10]; // per-warp record partials (group exchange)
+  double gc[NG][16];     // the tile's carries (group exchange)
+  double wpart[W][4];
+  unsigned int progress[NG];
+  SlotState ss;
+  double bcast[8];
+  double wred[W][16];
+  double gs[16];
+  uint8_t cflag[256];   // CTA range holds a stratum-first tile (grid <= 256)
+  int flag;
+  int need_exact, refresh, valued;
+  int cstar, cend;
+};
+
+template <bool FG>
+__host__ __device__ constexpr size_t smem_total() {
+  return 1024 + size_t(Geo<FG>::kS) * Geo<FG>::kStage + sizeof(Tail<FG>);
+}
+
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ double sgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// swizzled element addresses inside a staged tile: TMA boxes of 128-byte rows
+// (16 doubles / 32 codes) with 128B swizzle; a lane's 8-row thread-row is half
+// (exp(eta), G) or a quarter (codes) of a box row, and the lane pattern of the
+// consumers stays bank-conflict free.
+__device__ __forceinline__ double* e_at(unsigned char* base, int lr) {
+  return reinterpret_cast<double*>(base + swz<128>(lr * 8));
+}
+__device__ __forceinline__ uint32_t code_at(const unsigned char* base, int lr) {
+  return *reinterpret_cast<const uint32_t*>(base + swz<128>(lr * 4));
+}
+
+// coordinate_step (src/ccd.cpp:71-129), scalar, no FMA contraction.
+struct Step {
+  double new_beta, applied, new_hw;
+  bool skipped;
+};
+__device__ __noinline__ Step coordinate_step_dev(double beta_j, double grad, double hess, int kind,
+                                    double strength, bool penalized, double hw) {
+  double geff = grad, heff = hess;
+  bool at_zero_l1 = false;
+  if (penalized) {
+    if (kind == 2) {
+      geff = __dsub_rn(geff, __ddiv_rn(beta_j, strength));
+      heff = __dsub_rn(heff, __ddiv_rn(1.0, strength));
+    } else if (kind == 1) {
+      if (beta_j != 0.0)
+        geff = __dsub_rn(geff, __dmul_rn(strength, sgn(beta_j)));
+      else
+        at_zero_l1 = true;
+    }
+  }
+  Step s{beta_j, 0.0, hw, false};
+  if (at_zero_l1) {
+    if (fabs(geff) <= strength) {
+      s.new_hw = fmax(hw / 2.0, kHwFloor);
+      return s;
+    }
+    geff = __dsub_rn(geff, __dmul_rn(strength, sgn(geff)));
+  }
+  if (!(heff < 0.0)) {
+    if (geff != 0.0) {
+      s.skipped = true;
+      return s;
+    }
+    s.new_hw = fmax(hw / 2.0, kHwFloor);
+    return s;
+  }
+  double raw = __ddiv_rn(-geff, heff);
+  if (penalized && kind == 1 && beta_j != 0.0 && sgn(__dadd_rn(beta_j, raw)) != sgn(beta_j))
+    raw = -beta_j;
+  const double a = __dmul_rn(sgn(raw), fmin(fabs(raw), hw));
+  s.applied = a;
+  s.new_beta = __dadd_rn(beta_j, a);
+  s.new_hw = fmax(fmax(__dmul_rn(2.0, fabs(a)), hw / 2.0), kHwFloor);
+  return s;
+}
+
+// optional event trace: compiled in only with -DGSS_ENABLE_TRACE=1 (tools/trace_cycle.py;
+// build with GSS_TRACE_BUILD=1), and then active only when the engine was created with
+// GSS_TRACE=1
+#ifndef GSS_ENABLE_TRACE
+#define GSS_ENABLE_TRACE 0
+#endif
+constexpr unsigned kTrPerWarp = 1u << 16;  // events per traced warp (CTA 0 only)
+__device__ __forceinline__ unsigned& trace_slot(int warp) {
+  __shared__ unsigned tr_n[32];
+  return tr_n[warp];
+}
+// lane-0 only; no atomics: warp w of CTA 0 owns trace[w * kTrPerWarp ...]
+__device__ __forceinline__ void trace_ev(const CycleParams& P, int ev, int arg) {
+  if (!GSS_ENABLE_TRACE || !P.trace || blockIdx.x != 0) return;
+  const int warp = threadIdx.x >> 5;
+  unsigned& n = trace_slot(warp);
+  const unsigned i = atomicAdd(&n, 1u);  // smem atomic: several lanes may trace
+  if (i < kTrPerWarp) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    unsigned long long* o = P.trace + 2 * (size_t(warp) * kTrPerWarp + i);
+    o[0] = ns;
+    o[1] = (static_cast<unsigned long long>(ev) << 32) | static_cast<unsigned>(arg);
+  }
+}
+// per-CTA slot timestamps of ALL CTAs (trace build): region of warp 31, [slot][cta]
+__device__ __forceinline__ void trace_cta(const CycleParams& P, int ev, int slot, int region = 31) {
+  if (!GSS_ENABLE_TRACE || !P.trace) return;
+  const unsigned i = static_cast<unsigned>(slot) * gridDim.x + blockIdx.x;
+  if (i < kTrPerWarp) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    unsigned long long* o = P.trace + 2 * (size_t(region) * kTrPerWarp + i);
+    o[0] = ns;
+    o[1] = (static_cast<unsigned long long>(ev) << 32) | static_cast<unsigned>(blockIdx.x);
+  }
+}
+__device__ __forceinline__ void trace_c0(const CycleParams& P, int ev, int arg) {
+  trace_ev(P, ev, arg);
+}
+__device__ __forceinline__ void trace_w0(const CycleParams& P, int ev, int arg) {
+  if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == 0) trace_ev(P, ev, arg);
+}
+
+__device__ __forceinline__ bool gt0(int warp, int lane, int gw) {
+  return lane == 0 && (warp % gw) == 0;
+}
+
+// list entry i of a staged list (smem copy or global fallback)
+__device__ __forceinline__ int32_t list_at(const int32_t* ls, const ListRef& L, const int32_t* glob,
+                                           int i) {
+  return L.off >= 0 ? ls[L.off + i] : glob[L.lo + i];
+}
+
+// ---------------------------------------------------------------------------
+// grid barrier over the co-resident CTAs (monotonic counter, no reset)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned target) {
+  __threadfence();
+  atomicAdd(bar, 1u);
+  while (static_cast<int>(ld_acquire_u32(bar) - target) < 0) {
+  }
+  __threadfence();
+}
+
+// ---------------------------------------------------------------------------
+// per-slot kernel context
+// ---------------------------------------------------------------------------
+template <bool FG>
+struct Ctx {
+  const CycleParams* P;
+  unsigned char* smem;
+  Tail<FG>* tl;
+  int cta, t0, tc;         // tile range [t0, t0 + tc)
+  unsigned bar_target;     // next grid-barrier target
+  int par;                 // payload buffer parity
+};
+
+// ---------------------------------------------------------------------------
+// producer: streams every (slot, tile) position of this CTA through the ring
+// ---------------------------------------------------------------------------
+template <bool FG>
+__device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem, Tail<FG>* tl,
+                                      int t0, int tc, const CUtensorMap* tm_e,
+                                      const CUtensorMap* tm_code, const CUtensorMap* tm_g) {
+  using G = Geo<FG>;
+  const int lane = threadIdx.x & 31;
+  const long long total = static_cast<long long>(P.nslots) * tc;
+  const size_t nt1 = static_cast<size_t>(P.ntiles) + 1;
+  // waves of S positions: lane l < S owns position q0 + l (stage (q0 + l) % S), so
+  // every stage is awaited exactly one phase back and the S loads issue in parallel
+  for (long long q0 = 0; q0 < total; q0 += G::kS) {
+    const long long qq = q0 + lane;
+    if (lane < G::kS && qq < total) {
+      const int slot = static_cast<int>(qq / tc);
+      const int tile = t0 + static_cast<int>(qq % tc);
+      long long lo[3] = {0, 0, 0};
+      int cnt[3] = {0, 0, 0};
+      long long cols[3];
+      cols[0] = (P.mode == kModeCcd && slot > 0) ? P.slot_col[slot - 1] : -1;
+      cols[1] = P.slot_col[slot];
+      cols[2] = (slot + 1 < P.nslots) ? P.slot_col[slot + 1]
+                                      : (P.mode == kModeCcd ? P.slot_col[0] : -1);
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        if (cols[l] >= 0) {
+          const long long cb = P.col_ptr[cols[l]];
+          const uint32_t a = P.tile_ptr[size_t(cols[l]) * nt1 + tile];
+          const uint32_t b = P.tile_ptr[size_t(cols[l]) * nt1 + tile + 1];
+          lo[l] = cb + a;
+          cnt[l] = static_cast<int>(b - a);
+        }
+      }
+      const int s = static_cast<int>(qq % G::kS);
+      const uint32_t ph = static_cast<uint32_t>((qq / G::kS) & 1);
+      trace_c0(P, 24, static_cast<int>(qq));
+      while (!mbar_try_wait(&tl->empty[s], ph ^ 1)) {
+      }
+      trace_c0(P, 25, static_cast<int>(qq));
+      // the same tile of the previous slot must have committed its pending
+      // update before this slot's copy is read
+      if (qq >= tc) {
+        const long long prevq = qq - tc;
+        const int w = static_cast<int>((prevq % tc) % G::kNG);
+        const volatile unsigned* pr = &tl->progress[w];
+        while (static_cast<long long>(*pr) < prevq + 1) __nanosleep(32);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      trace_c0(P, 23, static_cast<int>(qq));
+      unsigned char* sb = smem + size_t(s) * G::kStage;
+      StageInfo& inf = tl->info[s];
+      inf.tile = tile;
+      inf.slot = slot;
+      uint32_t bytes = G::kEBytes + G::kCBytes + G::kGBytes;
+      int32_t* lbase = reinterpret_cast<int32_t*>(sb + G::kOffL);
+      uint32_t lbytes[3];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        inf.l[l].lo = lo[l];
+        inf.l[l].cnt = cnt[l];
+        lbytes[l] = 0;
+        if (cnt[l] > 0) {
+          const long long base = lo[l] & ~3LL;
+          const long long end = (lo[l] + cnt[l] + 3) & ~3LL;
+          if (end - base <= kNnzCap) {
+            inf.l[l].off = static_cast<int>(lo[l] - base);
+            lbytes[l] = static_cast<uint32_t>((end - base) * 4);
+            bytes += lbytes[l];
+          } else {
+            inf.l[l].off = -1;
+          }
+        } else {
+          inf.l[l].off = 0;
+        }
+      }
+      trace_c0(P, 20, static_cast<int>(qq));
+      mbar_arrive_expect_tx(&tl->full[s], bytes);
+      // 128-byte box rows: 16 doubles / 32 codes per row, 128B swizzle
+      tma_load_2d(sb, tm_e, 0, tile * (kTileRows / 16), &tl->full[s]);
+      tma_load_2d(sb + G::kOffC, tm_code, 0, tile * (kTileRows / 32), &tl->full[s]);
+      if constexpr (FG) tma_load_2d(sb + G::kOffG, tm_g, 0, tile * (kTileRows / 16), &tl->full[s]);
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+        if (lbytes[l])
+          bulk_load_1d(lbase + l * kNnzCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
+      trace_c0(P, 26, static_cast<int>(qq));
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// consumer: one tile of one slot, processed by a group of kGW warps
+// (warp gw of the group owns passes [gw*PPW, (gw+1)*PPW) of the tile)
+// ---------------------------------------------------------------------------
+template <int L>
+struct Lanes {
+  double v[L];
+};
+
+template <bool FG>
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + g), "r"(32 * Geo<FG>::kGW) : "memory");
+}
+
+// FUSED (Cox, CCD, indicator scan + next columns): the next slot's record
+// sums ride along the scan as two extra lanes (next-column e, and e on rows of
+// both columns), so the tile totals ARE the record.
+template <bool FG, bool IND, int KIND, bool FUSED = false>
+__device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl, unsigned char* sb,
+                                             const StageInfo& inf, const SlotState& ss, int g,
+                                             int gw, int lane, int par, double& acc0,
+                                             double& acc1, int& bad, uint64_t* empty_bar) {
+  using G = Geo<FG>;
+  constexpr int GW = G::kGW, PPW = kPasses / GW, GT = 32 * GW;
+  constexpr int NF = (KIND == kSlotLoglik) ? 1 : (IND ? 2 : 3);
+  constexpr int NU = FG ? NF : 0;
+  constexpr int NX = FUSED ? 2 : 0;
+  constexpr int L = NF + NU + NX;
+  static_assert(!FUSED || (!FG && IND && KIND == kSlotGrad), "fused records: Cox indicator only");
+  const int gt = gw * 32 + lane;  // thread index inside the group
+  const int t = inf.tile;
+  const long long row0 = static_cast<long long>(t) * kTileRows;
+  const unsigned char* sc = sb + G::kOffC;
+  const unsigned char* sg = sb + G::kOffG;
+  const int32_t* lbase = reinterpret_cast<const int32_t*>(sb + G::kOffL);
+  const int32_t* lp = lbase;
+  const int32_t* lcur = lbase + kNnzCap;
+  const int32_t* lnext = lbase + 2 * kNnzCap;
+  const ListRef& Lp = inf.l[0];
+  const ListRef& Lc = inf.l[1];
+  const ListRef& Ln = inf.l[2];
+  uint32_t* xm = tl->xm[g][par];
+  uint32_t* xn = tl->xn[g][par];
+  {  // the other buffers served the group's previous tile (released): clear them
+    uint32_t* om = tl->xm[g][par ^ 1];
+    uint32_t* on = tl->xn[g][par ^ 1];
+    for (int i = gt; i < 256; i += GT) {
+      om[i] = 0u;
+      on[i] = 0u;
+    }
+  }
+  const bool has_cur = KIND == kSlotGrad && ss.col >= 0;
+
+  // ---- tile carries -> group smem (visible after the first group barrier) ----
+  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = __ldcg(P.tcar + size_t(t) * kCarStride + lane);
+  const double* tcv = tl->gc[g];
+
+  // ---- stale tile after a refresh: reload exp(eta) from global ----
+  if (ss.refresh) {
+    for (int i = gt; i < kTileRows; i += GT) *e_at(sb, i) = __ldcg(P.e + row0 + i);
+  } else if (ss.pcol >= 0) {
+    // ---- patch + commit the pending update (src/engine.cpp:192-215) ----
+    for (int i = gt; i < Lp.cnt; i += GT) {
+      const int32_t r = list_at(lp, Lp, P.row_idx, i);
+      const int lr = static_cast<int>(r - row0);
+      if (code_at(sc, lr) & kCodeMasked) continue;
+      double* pe = e_at(sb, lr);
+      double en;
+      if (ss.pind) {
+        en = __dmul_rn(*pe, ss.phi);
+        red_add_f64(P.eta + r, ss.delta);  // xbeta_[i] += 1.0 * delta, fire-and-forget
+      } else {
+        const double ne = __dadd_rn(__ldcg(P.eta + r), __dmul_rn(P.vals[Lp.lo + i], ss.delta));
+        en = exp(ne);
+        P.eta[r] = ne;
+      }
+      *pe = en;
+      P.e[r] = en;
+    }
+  }
+  // ---- scan-column bitmask per thread-row (xm is all-zero on entry) ----
+  if (has_cur) {
+    for (int i = gt; i < Lc.cnt; i += GT) {
+      const int32_t r = list_at(lcur, Lc, P.row_idx, i);
+      const int lr = static_cast<int>(r - row0);
+      uint32_t w = 1u << (lr & 7);
+      if (!IND) {
+        const bool first =
+            i == 0 || ((list_at(lcur, Lc, P.row_idx, i - 1) - row0) >> 3) != (lr >> 3);
+        if (first) w |= static_cast<uint32_t>(i) << 8;
+      }
+      atomicOr(&xm[lr >> 3], w);
+    }
+  }
+  if constexpr (FUSED) {
+    for (int i = gt; i < Ln.cnt; i += GT) {
+      const int lr = static_cast<int>(list_at(lnext, Ln, P.row_idx, i) - row0);
+      atomicOr(&xn[lr >> 3], 1u << (lr & 7));
+    }
+  }
+  group_sync<FG>(g);
+  trace_w0(P, 10, t);
+
+  // per-row lane values of thread-row tr
+  struct Rows {
+    double ev[kIpt];
+    uint32_t cw[kIpt];
+    double gv[FG ? kIpt : 1], uv[FG ? kIpt : 1];
+    double xv[(KIND == kSlotGrad && !IND) ? kIpt : 1];
+    uint32_t xb, nb;
+  };
+  auto load_rows = [&](int tr, Rows& R) {
+#pragma unroll
+    for (int c = 0; c < kIpt / 2; ++c) {
+      const double2 v =
+          *reinterpret_cast<const double2*>(sb + swz<128>(tr * (kIpt * 8) + c * 16));
+      R.ev[2 * c] = v.x;
+      R.ev[2 * c + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < kIpt / 4; ++c) {
+      const uint4 v = *reinterpret_cast<const uint4*>(sc + swz<128>(tr * (kIpt * 4) + c * 16));
+      R.cw[4 * c] = v.x;
+      R.cw[4 * c + 1] = v.y;
+      R.cw[4 * c + 2] = v.z;
+      R.cw[4 * c + 3] = v.w;
+    }
+    if constexpr (FG) {
+#pragma unroll
+      for (int c = 0; c < kIpt / 2; ++c) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(sg + swz<128>(tr * (kIpt * 8) + c * 16));
+        R.gv[2 * c] = v.x;
+        R.gv[2 * c + 1] = v.y;
+      }
+#pragma unroll
+      for (int m = 0; m < kIpt; ++m) R.uv[m] = (R.cw[m] & kCodeCompeting) ? __drcp_rn(R.gv[m]) : 0.0;
+    }
+    R.xb = 0;
+    R.nb = 0;
+    if constexpr (FUSED) R.nb = xn[tr];
+    if constexpr (KIND == kSlotGrad) {
+      if (has_cur) R.xb = xm[tr];
+      if constexpr (!IND) {
+        const uint32_t bits = R.xb & 0xffu;
+        const long long k0 = Lc.lo + (R.xb >> 8);
+        int k = 0;
+#pragma unroll
+        for (int m = 0; m < kIpt; ++m) {
+          R.xv[m] = 0.0;
+          if ((bits >> m) & 1u) {
+            R.xv[m] = P.vals[k0 + k];
+            ++k;
+          }
+        }
+      }
+    }
+  };
+  auto row_val = [&](const Rows& R, int m) {
+    Lanes<L> rv;
+    rv.v[0] = R.ev[m];
+    if constexpr (NF >= 2) {
+      if constexpr (IND) {
+        rv.v[1] = ((R.xb >> m) & 1u) ? R.ev[m] : 0.0;
+      } else {
+        const double ex = __dmul_rn(R.ev[m], R.xv[m]);
+        rv.v[1] = ex;
+        rv.v[2] = __dmul_rn(ex, R.xv[m]);
+      }
+    }
+    if constexpr (FG) {
+#pragma unroll
+      for (int i = 0; i < NU; ++i) rv.v[NF + i] = __dmul_rn(R.uv[m], rv.v[i]);
+    }
+    if constexpr (FUSED) {
+      const bool nx = (R.nb >> m) & 1u;
+      rv.v[NF] = nx ? R.ev[m] : 0.0;                          // next column: e * x_next
+      rv.v[NF + 1] = (nx && ((R.xb >> m) & 1u)) ? R.ev[m] : 0.0;  // rows of both columns
+    }
+    return rv;
+  };
+  constexpr uint32_t kWork = (KIND == kSlotLoglik) ? (kCodeCount | kCodeEvent) : kCodeCount;
+
+  // ---- phase 1: thread aggregates of this warp's PPW passes ----
+  Lanes<L> st[PPW];
+  uint32_t work = 0;  // bit pp: this lane's rows of pass pp hold a block end (or event)
+#pragma unroll
+  for (int pp = 0; pp < PPW; ++pp) {
+    Rows R;
+    load_rows((gw * PPW + pp) * 32 + lane, R);
+#pragma unroll
+    for (int i = 0; i < L; ++i) st[pp].v[i] = 0.0;
+    uint32_t w = 0;
+#pragma unroll
+    for (int m = 0; m < kIpt; ++m) {
+      const Lanes<L> rv = row_val(R, m);
+#pragma unroll
+      for (int i = 0; i < L; ++i) st[pp].v[i] = __dadd_rn(st[pp].v[i], rv.v[i]);
+      w |= R.cw[m] & kWork;
+    }
+    if (w) work |= 1u << pp;
+  }
+  // ---- phase 2: warp inclusive scans (PPW interleaved) ----
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp) {
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const double o = __shfl_up_sync(0xffffffffu, st[pp].v[i], d);
+        if (lane >= d) st[pp].v[i] = __dadd_rn(o, st[pp].v[i]);
+      }
+    }
+  }
+  // exclusive prefix inside this warp's passes; warp total -> group exchange
+  Lanes<L> wt;
+#pragma unroll
+  for (int i = 0; i < L; ++i) wt.v[i] = 0.0;
+#pragma unroll
+  for (int pp = 0; pp < PPW; ++pp) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      double ex = __shfl_up_sync(0xffffffffu, st[pp].v[i], 1);
+      if (lane == 0) ex = 0.0;
+      const double tot = __shfl_sync(0xffffffffu, st[pp].v[i], 31);
+      st[pp].v[i] = __dadd_rn(wt.v[i], ex);
+      wt.v[i] = __dadd_rn(wt.v[i], tot);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) tl->gx[g][gw][i] = wt.v[i];
+  }
+  const unsigned wany = __reduce_or_sync(0xffffffffu, work);
+  group_sync<FG>(g);
+  // offset of this warp's passes inside the tile (fixed order) and the tile total
+  Lanes<L> off, ttot;
+#pragma unroll
+  for (int i = 0; i < L; ++i) off.v[i] = ttot.v[i] = 0.0;
+#pragma unroll
+  for (int w2 = 0; w2 < GW; ++w2) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const double x = tl->gx[g][w2][i];
+      if (w2 < gw) off.v[i] = __dadd_rn(off.v[i], x);
+      ttot.v[i] = __dadd_rn(ttot.v[i], x);
+    }
+  }
+  trace_w0(P, 11, t);
+
+  // ---- phase 3: transform at tied-block ends (Breslow), passes with work only ----
+  if (wany) {
+    double cf[NF], cr[NU > 0 ? NU : 1];
+    {
+      const double k1 = __dsub_rn(ss.phi, 1.0);
+      const bool reset_f = tcv[6] != 0.0;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        const int f = (NF == 2 && i == 1) ? 1 : i;  // IND: lanes (a, b)
+        double v = __dadd_rn(tcv[f], __dmul_rn(k1, tcv[3 + f]));
+        if (!reset_f) v = __dadd_rn(ss.cin_f[f], v);
+        cf[i] = v;
+      }
+      if constexpr (FG) {
+        const bool reset_r = tcv[14] != 0.0;
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+          const int f = (NU == 2 && i == 1) ? 1 : i;
+          double v = __dadd_rn(tcv[8 + f], __dmul_rn(k1, tcv[11 + f]));
+          if (!reset_r) v = __dadd_rn(v, ss.cin_r[f]);
+          cr[i] = v;  // u-weighted rows of this tile and the rest of the stratum
+        }
+      }
+    }
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp) {
+      if (!((wany >> pp) & 1u)) continue;
+      const int tr = (gw * PPW + pp) * 32 + lane;
+      Rows R;
+      load_rows(tr, R);
+      Lanes<L> run;
+#pragma unroll
+      for (int i = 0; i < L; ++i) run.v[i] = __dadd_rn(off.v[i], st[pp].v[i]);
+#pragma unroll
+      for (int m = 0; m < kIpt; ++m) {
+        const Lanes<L> rv = row_val(R, m);
+#pragma unroll
+        for (int i = 0; i < L; ++i) run.v[i] = __dadd_rn(run.v[i], rv.v[i]);
+        if (!(R.cw[m] & kWork)) continue;
+        if (KIND == kSlotLoglik && (R.cw[m] & kCodeEvent))
+          acc0 = __dadd_rn(acc0, __ldcg(P.eta + row0 + tr * kIpt + m));
+        const uint32_t d = R.cw[m] & kCodeCount;
+        if (!d) continue;
+        double den = __dadd_rn(cf[0], run.v[0]);
+        double n1 = 0.0, n2 = 0.0;
+        if constexpr (NF >= 2) {
+          n1 = __dadd_rn(cf[1], run.v[1]);
+          n2 = IND ? n1 : __dadd_rn(cf[NF - 1], run.v[NF - 1]);
+        }
+        if constexpr (FG) {
+          // u-weighted suffix strictly after this row, inside the stratum:
+          // S(k+1) = RcarryTot - inclusive in-tile prefix
+          const double gk = R.gv[m];
+          den = __dadd_rn(den, __dmul_rn(gk, __dsub_rn(cr[0], run.v[NF])));
+          if constexpr (NF >= 2) {
+            n1 = __dadd_rn(n1, __dmul_rn(gk, __dsub_rn(cr[1], run.v[NF + 1])));
+            if constexpr (!IND)
+              n2 = __dadd_rn(n2, __dmul_rn(gk, __dsub_rn(cr[NU - 1], run.v[NF + NU - 1])));
+            else
+              n2 = n1;
+          }
+        }
+        const double cnt = static_cast<double>(d);
+        if (!(den > 0.0)) {
+          bad = 1;
+        } else if constexpr (KIND == kSlotGrad) {
+          const double rinv = __drcp_rn(den);
+          const double Gm = __dmul_rn(n1, rinv);
+          const double Hm = IND ? Gm : __dmul_rn(n2, rinv);
+          acc0 = __dadd_rn(acc0, __dmul_rn(cnt, Gm));
+          acc1 = __dadd_rn(acc1, __dmul_rn(cnt, __dsub_rn(Hm, __dmul_rn(Gm, Gm))));
+        } else {
+          acc1 = __dadd_rn(acc1, __dmul_rn(cnt, log(den)));
+        }
+      }
+    }
+  }
+  trace_w0(P, 12, t);
+
+  // ---- the next slot's per-tile record (from the patched staged tile) ----
+  if constexpr (FUSED) {
+    if (gw == 0 && lane == 0) {
+      double* rec = P.trec + size_t(t) * kRecStride;
+      rec[kRa] = ttot.v[0];
+      rec[kRb] = ttot.v[NF];
+      rec[kRc] = ttot.v[NF];
+      rec[kRsa] = ttot.v[1];  // indicator scan column: its b lane is sum e over its rows
+      rec[kRsb] = ttot.v[NF + 1];
+      rec[kRsc] = ttot.v[NF + 1];
+    }
+  } else if (!(P.dbg & 2)) {
+    double rb = 0.0, rc = 0.0, rsa = 0.0, rsb = 0.0, rsc = 0.0;
+    double rub = 0.0, ruc = 0.0, rusa = 0.0, rusb = 0.0, rusc = 0.0;
+    const bool n_ind = ss.nind != 0;
+    const bool ccd_cur = P.mode == kModeCcd && has_cur;
+    for (int i = gt; i < Ln.cnt; i += GT) {
+      const int32_t r = list_at(lnext, Ln, P.row_idx, i);
+      const int lr = static_cast<int>(r - row0);
+      const double ev = *e_at(sb, lr);
+      const double x = n_ind ? 1.0 : P.vals[Ln.lo + i];
+      const double eb = __dmul_rn(ev, x);
+      const double ec = __dmul_rn(eb, x);
+      rb = __dadd_rn(rb, eb);
+      rc = __dadd_rn(rc, ec);
+      double u = 0.0;
+      if constexpr (FG) {
+        if (code_at(sc, lr) & kCodeCompeting)
+          u = __drcp_rn(*reinterpret_cast<const double*>(sg + swz<128>(lr * 8)));
+        rub = __dadd_rn(rub, __dmul_rn(u, eb));
+        ruc = __dadd_rn(ruc, __dmul_rn(u, ec));
+      }
+      if (ccd_cur && ((xm[lr >> 3] >> (lr & 7)) & 1u)) {
+        rsb = __dadd_rn(rsb, eb);
+        rsc = __dadd_rn(rsc, ec);
+        if constexpr (FG) {
+          rusb = __dadd_rn(rusb, __dmul_rn(u, eb));
+          rusc = __dadd_rn(rusc, __dmul_rn(u, ec));
+        }
+      }
+    }
+    if (ccd_cur) {
+      for (int i = gt; i < Lc.cnt; i += GT) {
+        const int32_t r = list_at(lcur, Lc, P.row_idx, i);
+        const int lr = static_cast<int>(r - row0);
+        const double ev = *e_at(sb, lr);
+        rsa = __dadd_rn(rsa, ev);
+        if constexpr (FG) {
+          if (code_at(sc, lr) & kCodeCompeting)
+            rusa = __dadd_rn(
+                rusa, __dmul_rn(__drcp_rn(*reinterpret_cast<const double*>(sg + swz<128>(lr * 8))),
+                                ev));
+        }
+      }
+    }
+    constexpr int NR = FG ? 10 : 5;
+    double rv[NR] = {rb, rc, rsa, rsb, rsc};
+    if constexpr (FG) {
+      rv[5] = rub;
+      rv[6] = ruc;
+      rv[7] = rusa;
+      rv[8] = rusb;
+      rv[9] = rusc;
+    }
+#pragma unroll
+    for (int i = 0; i < NR; ++i) rv[i] = warp_sum(rv[i]);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) tl->gr[g][gw][i] = rv[i];
+    }
+  }
+  if constexpr (!FUSED) group_sync<FG>(g);
+  if (!FUSED && gw == 0 && lane == 0 && !(P.dbg & 2)) {
+    constexpr int NR = FG ? 10 : 5;
+    double s[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) s[i] = 0.0;
+    for (int w2 = 0; w2 < GW; ++w2) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) s[i] = __dadd_rn(s[i], tl->gr[g][w2][i]);
+    }
+    double* rec = P.trec + size_t(t) * kRecStride;
+    rec[kRa] = ttot.v[0];
+    rec[kRb] = s[0];
+    rec[kRc] = s[1];
+    rec[kRsa] = s[2];
+    rec[kRsb] = s[3];
+    rec[kRsc] = s[4];
+    if constexpr (FG) {
+      rec[kRua] = ttot.v[NF];
+      rec[kRub] = s[5];
+      rec[kRuc] = s[6];
+      rec[kRusa] = s[7];
+      rec[kRusb] = s[8];
+      rec[kRusc] = s[9];
+    }
+  }
+  trace_w0(P, 13, t);
+}
+
+// returns true if the stage was already released (fused path)
+template <bool FG>
+__device__ __forceinline__ bool consume_tile(const CycleParams& P, Tail<FG>* tl, unsigned char* sb,
+                                             const StageInfo& inf, const SlotState& ss, int g,
+                                             int gw, int lane, int par, double& acc0,
+                                             double& acc1, int& bad, uint64_t* empty_bar) {
+  if constexpr (!FG) {
+    if (ss.fused) {
+      process_tile<false, true, kSlotGrad, true>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1,
+                                                 bad, empty_bar);
+      return false;
+    }
+  }
+  if (ss.kind == kSlotLoglik)
+    process_tile<FG, true, kSlotLoglik>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
+  else if (ss.cind)
+    process_tile<FG, true, kSlotGrad>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
+  else
+    process_tile<FG, false, kSlotGrad>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// records computed from global memory (launch prologue, refresh): for every
+// tile of the range, warp per tile.  Optional virtual pending update is not
+// needed here: callers commit first.
+// ---------------------------------------------------------------------------
+template <bool FG>
+__device__ __noinline__ void records_from_global(const CycleParams& P, int t0, int tc, long long ncol,
+                                    int warp, int lane) {
+  constexpr int W = Geo<FG>::kW;
+  const size_t nt1 = size_t(P.ntiles) + 1;
+  const bool n_ind = ncol >= 0 && (!P.has_vals || P.col_ind[ncol]);
+  for (int i = warp; i < tc; i += W) {
+    const int t = t0 + i;
+    const long long row0 = static_cast<long long>(t) * kTileRows;
+    double a = 0.0, ua = 0.0;
+    for (int k = lane; k < kTileRows; k += 32) {
+      const double ev = __ldcg(P.e + row0 + k);
+      a = __dadd_rn(a, ev);
+      if constexpr (FG) {
+        if (P.code[row0 + k] & kCodeCompeting) ua = __dadd_rn(ua, __dmul_rn(__drcp_rn(P.g[row0 + k]), ev));
+      }
+    }
+    double rb = 0.0, rc = 0.0, rub = 0.0, ruc = 0.0;
+    if (ncol >= 0) {
+      const long long cb = P.col_ptr[ncol];
+      const long long lo = cb + P.tile_ptr[size_t(ncol) * nt1 + t];
+      const long long hi = cb + P.tile_ptr[size_t(ncol) * nt1 + t + 1];
+      for (long long k = lo + lane; k < hi; k += 32) {
+        const int32_t r = P.row_idx[k];
+        const double ev = __ldcg(P.e + r);
+        const double x = n_ind ? 1.0 : P.vals[k];
+        const double eb = __dmul_rn(ev, x), ec = __dmul_rn(eb, x);
+        rb = __dadd_rn(rb, eb);
+        rc = __dadd_rn(rc, ec);
+        if constexpr (FG) {
+          if (P.code[r] & kCodeCompeting) {
+            const double u = __drcp_rn(P.g[r]);
+            rub = __dadd_rn(rub, __dmul_rn(u, eb));
+            ruc = __dadd_rn(ruc, __dmul_rn(u, ec));
+          }
+        }
+      }
+    }
+    a = warp_sum(a);
+    rb = warp_sum(rb);
+    rc = warp_sum(rc);
+    if constexpr (FG) {
+      ua = warp_sum(ua);
+      rub = warp_sum(rub);
+      ruc = warp_sum(ruc);
+    }
+    if (lane == 0) {
+      double* rec = P.trec + size_t(t) * kRecStride;
+      rec[kRa] = a;
+      rec[kRb] = rb;
+      rec[kRc] = rc;
+      rec[kRsa] = rec[kRsb] = rec[kRsc] = 0.0;
+      rec[kRua] = ua;
+      rec[kRub] = rub;
+      rec[kRuc] = ruc;
+      rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+    }
+  }
+}
+
+// In-kernel refresh (src/engine.cpp:120-160 via :217): the accepted update of
+// column `col` is applied to eta over this CTA's rows, then exp(eta) is
+// rebuilt for every row from the incrementally maintained eta (the eta drift
+// is a few ulps; load_beta()/refresh() API calls rebuild eta = X beta), and the
+// tile records are recomputed from the fresh values.  Returns max |eta|.
+template <bool FG>
+__device__ __noinline__ double refresh_tiles(const CycleParams& P, int t0, int tc, long long col, double delta,
+                                long long ncol, int warp, int lane) {
+  constexpr int W = Geo<FG>::kW;
+  const size_t nt1 = size_t(P.ntiles) + 1;
+  const bool c_ind = !P.has_vals || P.col_ind[col];
+  const bool n_ind = ncol >= 0 && (!P.has_vals || P.col_ind[ncol]);
+  double mx = 0.0;
+  for (int i = warp; i < tc; i += W) {
+    const int t = t0 + i;
+    const long long row0 = static_cast<long long>(t) * kTileRows;
+    {  // eta += x * delta over the tile's rows of the updated column
+      const long long cb = P.col_ptr[col];
+      const long long lo = cb + P.tile_ptr[size_t(col) * nt1 + t];
+      const long long hi = cb + P.tile_ptr[size_t(col) * nt1 + t + 1];
+      for (long long k = lo + lane; k < hi; k += 32) {
+        const int32_t r = P.row_idx[k];
+        if (P.code[r] & kCodeMasked) continue;
+        P.eta[r] = __dadd_rn(__ldcg(P.eta + r), __dmul_rn(c_ind ? 1.0 : P.vals[k], delta));
+      }
+      __syncwarp();
+      __threadfence_block();
+    }
+    double a = 0.0, ua = 0.0;
+#pragma unroll 4
+    for (int k = lane; k < kTileRows; k += 32) {
+      const long long r = row0 + k;
+      const uint32_t cw = P.code[r];
+      if (cw & kCodeMasked) continue;
+      const double et = __ldcg(P.eta + r);
+      const double ev = exp(et);
+      P.e[r] = ev;
+      mx = fmax(mx, fabs(et));
+      a = __dadd_rn(a, ev);
+      if constexpr (FG) {
+        if (cw & kCodeCompeting) ua = __dadd_rn(ua, __dmul_rn(__drcp_rn(P.g[r]), ev));
+      }
+    }
+    __syncwarp();
+    __threadfence_block();
+    double rb = 0.0, rc = 0.0, rub = 0.0, ruc = 0.0;
+    if (ncol >= 0) {
+      const long long cb = P.col_ptr[ncol];
+      const long long lo = cb + P.tile_ptr[size_t(ncol) * nt1 + t];
+      const long long hi = cb + P.tile_ptr[size_t(ncol) * nt1 + t + 1];
+      for (long long k = lo + lane; k < hi; k += 32) {
+        const int32_t r = P.row_idx[k];
+        const double ev = __ldcg(P.e + r);
+        const double x = n_ind ? 1.0 : P.vals[k];
+        const double eb = __dmul_rn(ev, x), ec = __dmul_rn(eb, x);
+        rb = __dadd_rn(rb, eb);
+        rc = __dadd_rn(rc, ec);
+        if constexpr (FG) {
+          if (P.code[r] & kCodeCompeting) {
+            const double u = __drcp_rn(P.g[r]);
+            rub = __dadd_rn(rub, __dmul_rn(u, eb));
+            ruc = __dadd_rn(ruc, __dmul_rn(u, ec));
+          }
+        }
+      }
+    }
+    a = warp_sum(a);
+    rb = warp_sum(rb);
+    rc = warp_sum(rc);
+    if constexpr (FG) {
+      ua = warp_sum(ua);
+      rub = warp_sum(rub);
+      ruc = warp_sum(ruc);
+    }
+    if (lane == 0) {
+      double* rec = P.trec + size_t(t) * kRecStride;
+      rec[kRa] = a;
+      rec[kRb] = rb;
+      rec[kRc] = rc;
+      rec[kRsa] = rec[kRsb] = rec[kRsc] = 0.0;
+      rec[kRua] = ua;
+      rec[kRub] = rub;
+      rec[kRuc] = ruc;
+      rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+    }
+  }
+  return mx;
+}
+
+// Sparse correction of the records for a VALUED pending update (exp is not
+// linear in delta): rec += sum over the pending rows of (e_new - e_old) terms.
+template <bool FG>
+__device__ __noinline__ void correct_records_valued(const CycleParams& P, int t0, int tc, long long pcol,
+                                       double delta, long long ncol, int warp, int lane) {
+  constexpr int W = Geo<FG>::kW;
+  const size_t nt1 = size_t(P.ntiles) + 1;
+  const bool n_ind = ncol >= 0 && (!P.has_vals || P.col_ind[ncol]);
+  for (int i = warp; i < tc; i += W) {
+    const int t = t0 + i;
+    const long long cb = P.col_ptr[pcol];
+    const long long lo = cb + P.tile_ptr[size_t(pcol) * nt1 + t];
+    const long long hi = cb + P.tile_ptr[size_t(pcol) * nt1 + t + 1];
+    long long nlo = 0, nhi = 0;
+    if (ncol >= 0) {
+      const long long nb = P.col_ptr[ncol];
+      nlo = nb + P.tile_ptr[size_t(ncol) * nt1 + t];
+      nhi = nb + P.tile_ptr[size_t(ncol) * nt1 + t + 1];
+    }
+    double da = 0.0, db = 0.0, dc = 0.0, dua = 0.0, dub = 0.0, duc = 0.0;
+    for (long long k = lo + lane; k < hi; k += 32) {
+      const int32_t r = P.row_idx[k];
+      if (P.code[r] & kCodeMasked) continue;
+      const double eo = __ldcg(P.e + r);
+      const double en = exp(__dadd_rn(__ldcg(P.eta + r), __dmul_rn(P.vals[k], delta)));
+      const double de = __dsub_rn(en, eo);
+      double u = 0.0;
+      if constexpr (FG) {
+        if (P.code[r] & kCodeCompeting) u = __drcp_rn(P.g[r]);
+      }
+      da = __dadd_rn(da, de);
+      if constexpr (FG) dua = __dadd_rn(dua, __dmul_rn(u, de));
+      // is r also a row of the next column?
+      long long a = nlo, b = nhi;
+      while (a < b) {
+        const long long mid = (a + b) >> 1;
+        if (P.row_idx[mid] < r)
+          a = mid + 1;
+        else
+          b = mid;
+      }
+      if (a < nhi && P.row_idx[a] == r) {
+        const double x = n_ind ? 1.0 : P.vals[a];
+        const double eb = __dmul_rn(de, x), ec = __dmul_rn(eb, x);
+        db = __dadd_rn(db, eb);
+        dc = __dadd_rn(dc, ec);
+        if constexpr (FG) {
+          dub = __dadd_rn(dub, __dmul_rn(u, eb));
+          duc = __dadd_rn(duc, __dmul_rn(u, ec));
+        }
+      }
+    }
+    da = warp_sum(da);
+    db = warp_sum(db);
+    dc = warp_sum(dc);
+    if constexpr (FG) {
+      dua = warp_sum(dua);
+      dub = warp_sum(dub);
+      duc = warp_sum(duc);
+    }
+    if (lane == 0) {
+      double* rec = P.trec + size_t(t) * kRecStride;
+      rec[kRa] = __dadd_rn(rec[kRa], da);
+      rec[kRb] = __dadd_rn(rec[kRb], db);
+      rec[kRc] = __dadd_rn(rec[kRc], dc);
+      rec[kRsa] = rec[kRsb] = rec[kRsc] = 0.0;
+      if constexpr (FG) {
+        rec[kRua] = __dadd_rn(rec[kRua], dua);
+        rec[kRub] = __dadd_rn(rec[kRub], dub);
+        rec[kRuc] = __dadd_rn(rec[kRuc], duc);
+        rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+      }
+    }
+  }
+}
+
+// Exact validate-before-mutate over this CTA's rows (src/engine.cpp:171-190).
+__device__ __noinline__ int validate_rows(const CycleParams& P, int t0, int tc, long long col, double delta,
+                             int tid, int nthr) {
+  const size_t nt1 = size_t(P.ntiles) + 1;
+  const long long cb = P.col_ptr[col];
+  const long long lo = cb + P.tile_ptr[size_t(col) * nt1 + t0];
+  const long long hi = cb + P.tile_ptr[size_t(col) * nt1 + t0 + tc];
+  const bool ind = !P.has_vals || P.col_ind[col];
+  int over = 0;
+  for (long long k = lo + tid; k < hi; k += nthr) {
+    const int32_t r = P.row_idx[k];
+    if (P.code[r] & kCodeMasked) continue;
+    const double x = ind ? 1.0 : P.vals[k];
+    if (fabs(__dadd_rn(__ldcg(P.eta + r), __dmul_rn(x, delta))) > kXbetaBound) over = 1;
+  }
+  return over;
+}
+
+// ---------------------------------------------------------------------------
+// In-range segmented scans of the per-tile records (warp 0): per-tile carries
+// (uncorrected value + s-part) and the CTA payload aggregates.
+// ---------------------------------------------------------------------------
+template <bool FG>
+__device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, double* pay, int lane) {
+  // forward: exclusive segmented prefix, flags at stratum-first tiles
+  double carry[6] = {0, 0, 0, 0, 0, 0};
+  int seen = 0;  // a stratum-first tile was passed inside the range
+  for (int ch = 0; ch < tc; ch += 32) {
+    const int i = ch + lane;
+    const bool valid = i < tc;
+    const int t = t0 + i;
+    double v[6];
+    int f = 0;
+    if (valid) {
+      const double* rec = P.trec + size_t(t) * kRecStride;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) v[k] = __ldcg(rec + k);
+      f = P.tile_first[t] ? 1 : 0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) v[k] = 0.0;
+    }
+    // segmented inclusive scan (x earlier, y later): y.f ? y.v : x.v + y.v
+    int sf = f;
+    double s[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s[k] = v[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int of = __shfl_up_sync(0xffffffffu, sf, d);
+      double o[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) o[k] = __shfl_up_sync(0xffffffffu, s[k], d);
+      if (lane >= d) {
+        if (!sf) {
+#pragma unroll
+          for (int k = 0; k < 6; ++k) s[k] = __dadd_rn(o[k], s[k]);
+        }
+        sf |= of;
+      }
+    }
+    // exclusive: previous lane's inclusive, combined after the chunk carry
+    int ef = __shfl_up_sync(0xffffffffu, sf, 1);
+    double ex[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) ex[k] = __shfl_up_sync(0xffffffffu, s[k], 1);
+    if (lane == 0) {
+      ef = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ex[k] = 0.0;
+    }
+    double outv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) outv[k] = ef ? ex[k] : __dadd_rn(carry[k], ex[k]);
+    const int reset = seen | ef | f;
+    if (f) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) outv[k] = 0.0;
+    }
+    if (valid) {
+      double* tcp = P.tcar + size_t(t) * kCarStride;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) tcp[k] = outv[k];
+      tcp[6] = reset ? 1.0 : 0.0;
+    }
+    // chunk total -> carry
+    const int last = min(31, tc - ch - 1);
+    const int tf = __shfl_sync(0xffffffffu, sf, last);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double tv = __shfl_sync(0xffffffffu, s[k], last);
+      carry[k] = tf ? tv : __dadd_rn(carry[k], tv);
+    }
+    seen |= tf;
+  }
+  if (lane == 0) {
+    pay[3] = seen ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) pay[4 + k] = carry[k];
+  }
+  if constexpr (FG) {
+    // reverse: inclusive segmented suffix; element i is cut from i+1 when
+    // tile i+1 starts a stratum
+    double rc[6] = {0, 0, 0, 0, 0, 0};
+    int rseen = 0;  // a stratum-first tile lies after the current position
+    const int nch = (tc + 31) / 32;
+    for (int cc = nch - 1; cc >= 0; --cc) {
+      const int ch = cc * 32;
+      const int i = ch + 31 - lane;  // lane 0 = highest tile of the chunk
+      const bool valid = i < tc;
+      const int t = t0 + i;
+      double v[6];
+      int fnext = 0;  // tile i+1 (inside the range) starts a stratum
+      if (valid) {
+        const double* rec = P.trec + size_t(t) * kRecStride;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = __ldcg(rec + 6 + k);
+        fnext = (i + 1 < tc && P.tile_first[t + 1]) ? 1 : 0;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = 0.0;
+      }
+      int sf = fnext;
+      double s[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s[k] = v[k];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int of = __shfl_up_sync(0xffffffffu, sf, d);
+        double o[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) o[k] = __shfl_up_sync(0xffffffffu, s[k], d);
+        if (lane >= d) {
+          if (!sf) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s[k] = __dadd_rn(o[k], s[k]);
+          }
+          sf |= of;
+        }
+      }
+      // inclusive value at tile i, plus the carry from higher chunks unless cut
+      double outv[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) outv[k] = sf ? s[k] : __dadd_rn(rc[k], s[k]);
+      const int reset = sf | rseen;
+      if (valid) {
+        double* tcp = P.tcar + size_t(t) * kCarStride;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) tcp[8 + k] = outv[k];
+        tcp[14] = reset ? 1.0 : 0.0;
+      }
+      // carry for the next (lower) chunk: the value at the chunk's lowest valid tile
+      const int lowest = 31 - 0;  // lane holding i = ch (always valid)
+      const int lf = __shfl_sync(0xffffffffu, sf, lowest);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const double tv = __shfl_sync(0xffffffffu, s[k], lowest);
+        rc[k] = lf ? tv : __dadd_rn(rc[k], tv);
+      }
+      rseen |= lf;
+      // a stratum start at the chunk's lowest tile cuts everything below it
+      const int low_first = P.tile_first[t0 + ch] ? 1 : 0;
+      if (low_first) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rc[k] = 0.0;
+        rseen = 1;
+      }
+    }
+    // head = rows before the first stratum-first tile of the range
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) pay[10 + k] = rc[k];
+    }
+  }
+}
+
+// All consumer threads read the published payloads once (thread c <- CTA c)
+// and reduce them with a fixed tree: the slot partials over all CTAs (the same
+// tree in every CTA => identical results everywhere), the fwd tails of CTAs
+// [cstar, cta) and the rev heads of CTAs (cta, cend] (segmented by strata).
+// Result: tl->gs[0..2] partials, [3..8] fwd (a,b,c,sa,sb,sc), [9..14] rev.
+template <bool FG>
+__device__ __noinline__ void gather_payloads(const CycleParams& P, const double* pay_all, int cta, int cstar,
+                                int cend, Tail<FG>* tl, int tid) {
+  constexpr int W = Geo<FG>::kW, NC = 32 * W, NV = FG ? 15 : 9;
+  const int warp = tid >> 5, lane = tid & 31;
+  double v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = 0.0;
+  for (int c = tid; c < P.grid; c += NC) {
+    const double* py = pay_all + size_t(c) * kPayStride;
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < (FG ? 16 : 10); ++i) x[i] = __ldcg(py + i);
+    v[0] = __dadd_rn(v[0], x[0]);
+    v[1] = __dadd_rn(v[1], x[1]);
+    v[2] = __dadd_rn(v[2], x[2]);
+    if (c >= cstar && c < cta) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) v[3 + i] = __dadd_rn(v[3 + i], x[4 + i]);
+    }
+    if constexpr (FG) {
+      if (c > cta && c <= cend) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) v[9 + i] = __dadd_rn(v[9 + i], x[10 + i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tl->wred[warp][i] = v[i];
+  }
+  consumer_sync(NC);
+  if (tid == 0) {
+#pragma unroll 1
+    for (int i = 0; i < NV; ++i) {
+      double r = 0.0;
+      for (int w = 0; w < W; ++w) r = __dadd_rn(r, tl->wred[w][i]);
+      tl->gs[i] = r;
+    }
+  }
+  consumer_sync(NC);
+}
+
+// corrected CTA carries from the gathered sums (thread 0)
+template <bool FG>
+__device__ __forceinline__ void set_carry_in(Tail<FG>* tl, double k1) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tl->ss.cin_f[i] = __dadd_rn(tl->gs[3 + i], __dmul_rn(k1, tl->gs[6 + i]));
+  if constexpr (FG) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      tl->ss.cin_r[i] = __dadd_rn(tl->gs[9 + i], __dmul_rn(k1, tl->gs[12 + i]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the persistent cycle kernel
+// ---------------------------------------------------------------------------
+template <bool FG>
+__global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
+    cycle_kernel(const __grid_constant__ CUtensorMap tm_e,
+                 const __grid_constant__ CUtensorMap tm_code,
+                 const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CycleParams P) {
+  using Gm = Geo<FG>;
+  constexpr int W = Gm::kW, S = Gm::kS;
+  constexpr int NC = 32 * W;  // consumer threads
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  Tail<FG>* tl = reinterpret_cast<Tail<FG>*>(smem + size_t(S) * Gm::kStage);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  const int G = P.grid;
+  auto range_lo = [&](int c) {
+    return static_cast<int>((static_cast<long long>(c) * P.ntiles) / G);
+  };
+  const int t0 = range_lo(cta);
+  const int tc = range_lo(cta + 1) - t0;
+  Ctl* ctl = P.ctl;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&tl->full[s], 1);
+      mbar_init(&tl->empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (tid < Gm::kNG) tl->progress[tid] = 0u;
+  if (tid < 32) trace_slot(tid) = 0u;
+  for (int i = tid; i < Gm::kNG * 512; i += blockDim.x) {
+    (&tl->xm[0][0][0])[i] = 0u;
+    (&tl->xn[0][0][0])[i] = 0u;
+  }
+  // static stratum flags of every CTA range (carry segmentation bounds)
+  for (int c = tid; c < G; c += blockDim.x) {
+    uint8_t f = 0;
+    for (int t = range_lo(c); t < range_lo(c + 1); ++t) f |= P.tile_first[t];
+    tl->cflag[c] = f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int cs = 0;
+    for (int c = cta - 1; c >= 0; --c)
+      if (tl->cflag[c]) {
+        cs = c;
+        break;
+      }
+    int ce = G - 1;
+    for (int c = cta + 1; c < G; ++c)
+      if (tl->cflag[c]) {
+        ce = c;
+        break;
+      }
+    tl->cstar = cs;
+    tl->cend = ce;
+  }
+
+  if (warp == W) {
+    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g);
+    return;
+  }
+
+  // ------------------------- consumer / control warps ----------------------
+  // replicated CCD state (identical in every CTA: same inputs, same order)
+  unsigned bar_target = static_cast<unsigned>(ctl->bar_base);
+  double absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
+  double slack = ctl->bound_slack;
+  long long accepted = ctl->accepted, refreshes = ctl->refreshes, skipped = ctl->skipped;
+  int err = ctl->err_code;
+  long long err_col = ctl->err_col;
+  const bool rec_ok = P.mode == kModeCcd && ctl->rec_valid && ctl->rec_col == P.slot_col[0];
+  SlotState& ss = tl->ss;
+  consumer_sync(NC);
+  const int cstar = tl->cstar, cend = tl->cend;
+
+  // payload double buffer, indexed by the exchange count
+  int xi = 0;
+  auto wbuf = [&]() { return P.cpay + (size_t(xi & 1) * G + cta) * kPayStride; };
+  auto rbuf = [&](int x) { return P.cpay + size_t(x & 1) * G * kPayStride; };
+  int xtr = 0;  // exchange ordinal (trace)
+  // CTA barrier first (orders every thread's writes before thread 0), then one
+  // gpu-scope fence + release by thread 0 (the cooperative-groups grid.sync pattern)
+  auto exchange = [&]() {
+    consumer_sync(NC);
+    if (tid == 0) {
+      trace_cta(P, 31, xtr, 29);
+      bar_target += static_cast<unsigned>(G);
+      grid_arrive_wait(P.bar, bar_target);
+      trace_cta(P, 32, xtr, 30);
+      ++xtr;
+    }
+    ++xi;
+    consumer_sync(NC);
+  };
+  // publish this CTA's range aggregates (+ optional extras), exchange, gather
+  auto publish_exchange_gather = [&](double p0, double p1, double pb) {
+    if (warp == 0) {
+      double* pm = wbuf();
+      range_scan<FG>(P, t0, tc, pm, lane);
+      if (lane == 0) {
+        pm[0] = p0;
+        pm[1] = p1;
+        pm[2] = pb;
+      }
+    }
+    exchange();
+    gather_payloads<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, tid);
+  };
+
+  // ---- prologue: records for slot 0 and the slot-0 carries ----
+  if (!rec_ok) records_from_global<FG>(P, t0, tc, P.slot_col[0], warp, lane);
+  __threadfence();
+  consumer_sync(NC);
+  publish_exchange_gather(0.0, 0.0, 0.0);
+  if (tid == 0) {
+    set_carry_in<FG>(tl, 0.0);
+    ss.pcol = -1;
+    ss.delta = 0.0;
+    ss.phi = 1.0;
+    ss.pind = 1;
+    ss.refresh = 0;
+    ss.dry = err ? 1 : 0;
+  }
+
+  long long qbase = 0;  // stream position of the slot's first tile
+  int gpar = 0;         // this warp's group: mask buffer of its next tile
+  for (int k = 0; k < P.nslots; ++k) {
+    const long long col = P.slot_col[k];
+    const long long ncol =
+        (k + 1 < P.nslots) ? P.slot_col[k + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
+    // step inputs, loaded now and used after the exchange (latency hidden)
+    double in_fixed = 0.0, in_beta = 0.0, in_hw = 0.0, in_cmax = 0.0;
+    int in_pen = 0, in_ind = 1;
+    if (tid == 0 && col >= 0) {
+      in_fixed = __ldcg(P.fixed + col);
+      in_beta = __ldcg(P.beta + col);
+      in_hw = __ldcg(P.halfwidth + col);
+      in_cmax = __ldcg(P.colmax + col);
+      in_pen = P.penalized[col];
+      in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
+      ss.col = col;
+      ss.kind = kSlotGrad;
+      ss.cind = in_ind;
+    } else if (tid == 0) {
+      ss.col = col;
+      ss.kind = kSlotLoglik;
+      ss.cind = 1;
+    }
+    if (tid == 0) {
+      ss.nind = ncol >= 0 ? ((!P.has_vals || P.col_ind[ncol]) ? 1 : 0) : 1;
+      ss.fused = (!FG && P.mode == kModeCcd && col >= 0 && ncol >= 0 && ss.cind && ss.nind &&
+                  !(P.dbg & 8)) ? 1 : 0;
+    }
+    consumer_sync(NC);
+    // ---- consume this CTA's tiles of slot k (warp per tile, fixed order) ----
+    double acc0 = 0.0, acc1 = 0.0;
+    int bad = 0;
+    const bool dry = ss.dry != 0;
+    {
+      constexpr int NGr = Gm::kNG, GWr = Gm::kGW;
+      const int g = warp / GWr, gw = warp % GWr;
+      // Progress (the producer's licence to reload a tile for the next slot) is
+      // published one tile late: the proxy fence ordering this tile's commits
+      // before that TMA read runs when the group starts its next tile, by which
+      // time the commit stores have drained; the slot's last tile is flushed below.
+      long long pend_q = -1;
+      for (int i = g; i < tc; i += NGr) {
+        const long long q = qbase + i;
+        const int s = static_cast<int>(q % S);
+        const uint32_t ph = static_cast<uint32_t>((q / S) & 1);
+        mbar_wait(&tl->full[s], ph);
+        if (gt0(warp, lane, GWr)) trace_c0(P, 21, static_cast<int>(q));
+        if (pend_q >= 0) {
+          fence_proxy_async_global();
+          group_sync<FG>(g);
+          if (gw == 0 && lane == 0)
+            *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) =
+                static_cast<unsigned>(pend_q + 1);
+        }
+        unsigned char* sb = smem + size_t(s) * Gm::kStage;
+        bool released = false;
+        if (!dry && !(P.dbg & 1))
+          released = consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1,
+                                      bad, &tl->empty[s]);
+        gpar ^= 1;
+        group_sync<FG>(g);
+        if (gw == 0 && lane == 0) {
+          trace_c0(P, 22, static_cast<int>(q));
+          if (!released) mbar_arrive(&tl->empty[s]);
+        }
+        pend_q = q;
+      }
+      if (pend_q >= 0) {
+        fence_proxy_async_global();
+        group_sync<FG>(g);
+        if (gw == 0 && lane == 0)
+          *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = static_cast<unsigned>(pend_q + 1);
+      }
+    }
+    qbase += tc;
+    acc0 = warp_sum(acc0);
+    acc1 = warp_sum(acc1);
+    const double badw = warp_sum(static_cast<double>(bad));
+    if (lane == 0) {
+      tl->wpart[warp][0] = acc0;
+      tl->wpart[warp][1] = acc1;
+      tl->wpart[warp][2] = badw;
+    }
+    consumer_sync(NC);
+    if (tid == 0) {
+      trace_c0(P, 3, k);
+      trace_cta(P, 30, k);
+    }
+    if (P.dbg & 16) continue;  // ablation: stream only
+    // ---- publish partials + range aggregates, exchange, gather ----
+    {
+      double r0 = 0.0, r1 = 0.0, rb = 0.0;
+      if (tid == 0) {
+        for (int w = 0; w < W; ++w) {
+          r0 = __dadd_rn(r0, tl->wpart[w][0]);
+          r1 = __dadd_rn(r1, tl->wpart[w][1]);
+          rb = __dadd_rn(rb, tl->wpart[w][2]);
+        }
+        trace_c0(P, 7, k);
+      }
+      publish_exchange_gather(r0, r1, rb);
+    }
+    if (tid == 0) trace_c0(P, 4, k);
+    // ---- finish + coordinate step (thread 0 of every CTA, replicated) ----
+    if (tid == 0) {
+      const double r0 = tl->gs[0], r1 = tl->gs[1];
+      const bool badden = tl->gs[2] != 0.0;
+      double delta = 0.0;
+      int need_exact = 0;
+      if (!dry) {
+        if (col < 0) {
+          const double ll = __dsub_rn(r0, r1);
+          if (badden && !err) {
+            err = kErrNonPos;
+            err_col = -1;
+          }
+          if (cta == 0) {
+            ctl->ll_fixed = r0;
+            ctl->ll_logden = r1;
+            ctl->loglik = ll;
+            if (P.slot_out) P.slot_out[size_t(k) * 4 + 3] = ll;
+          }
+        } else {
+          // Engine::finish (src/engine.cpp:220-230)
+          const double grad = __dsub_rn(in_fixed, r0);
+          double hess = -r1;
+          if (hess > 0.0) hess = 0.0;
+          const bool nonfinite = !isfinite(grad) || !isfinite(hess);
+          if (cta == 0) {
+            ctl->grad_sum = r0;
+            ctl->hess_sum = r1;
+            ctl->gradient = grad;
+            ctl->hessian = hess;
+            ctl->fixed_term = in_fixed;
+            if (P.slot_out) {
+              P.slot_out[size_t(k) * 4 + 0] = grad;
+              P.slot_out[size_t(k) * 4 + 1] = hess;
+              P.slot_out[size_t(k) * 4 + 2] = in_fixed;
+            }
+          }
+          if (badden || nonfinite) {
+            if (!err) {
+              err = kErrNonPos;
+              err_col = col;
+            }
+          } else if (P.mode == kModeCcd && !err) {
+            // coordinate_step + update decision (src/ccd.cpp:152-167)
+            const Step stp = coordinate_step_dev(in_beta, grad, hess, P.pen_kind, P.pen_strength,
+                                                 in_pen != 0, in_hw);
+            if (stp.skipped) {
+              ++skipped;
+            } else {
+              if (cta == 0) P.halfwidth[col] = stp.new_hw;
+              if (stp.applied != 0.0) {
+                const double step_slack = __dmul_rn(in_cmax, fabs(stp.applied));
+                delta = stp.applied;
+                // fast validate: max|eta| at the last refresh/load plus the
+                // accumulated |delta|*max|x| bounds every row
+                need_exact = (absmax + slack + step_slack <= kFastBound) ? 0 : 1;
+                tl->bcast[5] = step_slack;
+              }
+            }
+          }
+        }
+      }
+      tl->bcast[3] = delta;
+      tl->need_exact = need_exact;
+      // provisional carries for slot k+1 (linear path)
+      set_carry_in<FG>(tl, (delta != 0.0) ? __dsub_rn(exp(delta), 1.0) : 0.0);
+    }
+    consumer_sync(NC);
+    double delta = tl->bcast[3];
+    // ---- exact validate-before-mutate (rare): one more exchange ----
+    if (tl->need_exact) {
+      if (tid == 0) tl->flag = 0;
+      consumer_sync(NC);
+      if (validate_rows(P, t0, tc, col, delta, tid, NC)) tl->flag = 1;
+      consumer_sync(NC);
+      if (tid == 0) wbuf()[17] = tl->flag ? 1.0 : 0.0;
+      exchange();
+      if (tid == 0) {
+        const double* pa = rbuf(xi - 1);
+        bool any = false;
+        for (int c = 0; c < G; ++c) any |= __ldcg(pa + size_t(c) * kPayStride + 17) != 0.0;
+        if (any) {
+          if (!err) {
+            err = kErrOverflow;
+            err_col = col;
+          }
+          if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
+          tl->bcast[3] = 0.0;
+        }
+      }
+      consumer_sync(NC);
+      delta = tl->bcast[3];
+    }
+    // ---- accept: beta_[column] += delta, refresh cadence (src/engine.cpp:216-217) ----
+    if (tid == 0) {
+      int do_refresh = 0;
+      if (delta != 0.0) {
+        if (cta == 0) P.beta[col] = __dadd_rn(in_beta, delta);
+        slack = __dadd_rn(slack, tl->bcast[5]);
+        ++accepted;
+        if (accepted % P.recompute_interval == 0) {
+          do_refresh = 1;  // refresh subsumes the incremental update
+          ++refreshes;
+        }
+      }
+      tl->refresh = do_refresh;
+      tl->valued = (delta != 0.0 && !do_refresh && !in_ind) ? 1 : 0;
+    }
+    consumer_sync(NC);
+    if (tl->refresh) {
+      const double mx = refresh_tiles<FG>(P, t0, tc, col, delta, ncol, warp, lane);
+      fence_proxy_async_global();
+      double m = mx;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+      if (lane == 0) tl->wpart[warp][3] = m;
+      __threadfence();
+      consumer_sync(NC);
+      if (tid == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < W; ++w) mm = fmax(mm, tl->wpart[w][3]);
+        wbuf()[16] = mm;
+      }
+      publish_exchange_gather(0.0, 0.0, 0.0);
+      if (tid == 0) {
+        set_carry_in<FG>(tl, 0.0);
+        const double* pa = rbuf(xi - 1);
+        double mm = 0.0;
+        for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayStride + 16));
+        absmax = mm;  // the bound is exact again
+        slack = 0.0;
+      }
+    } else if (tl->valued) {
+      correct_records_valued<FG>(P, t0, tc, col, delta, ncol, warp, lane);
+      __threadfence();
+      consumer_sync(NC);
+      publish_exchange_gather(0.0, 0.0, 0.0);
+      if (tid == 0) set_carry_in<FG>(tl, 0.0);
+    }
+    if (tid == 0) {
+      ss.pcol = (delta != 0.0 && !tl->refresh) ? col : -1;
+      ss.delta = delta;
+      ss.phi = (delta != 0.0) ? exp(delta) : 1.0;
+      ss.pind = in_ind;
+      ss.refresh = tl->refresh;
+      ss.dry = err ? 1 : 0;
+      trace_c0(P, 5, k);
+    }
+    consumer_sync(NC);
+  }
+
+  // ---- epilogue: CTA 0 persists the replicated state ----
+  if (tid == 0 && cta == 0) {
+    ctl->bar_base = bar_target;
+    ctl->eta_absmax_bits = static_cast<unsigned long long>(__double_as_longlong(absmax));
+    ctl->bound_slack = slack;
+    ctl->accepted = accepted;
+    ctl->refreshes = refreshes;
+    ctl->skipped = skipped;
+    ctl->err_code = err;
+    ctl->err_col = err_col;
+    ctl->rec_valid = (P.mode == kModeCcd && !err) ? 1 : 0;
+    ctl->rec_col = P.slot_col[0];
+  }
+}
+
+}  // namespace
+
+size_t cycle_smem_bytes(bool weighted) {
+  return weighted ? smem_total<true>() : smem_total<false>();
+}
+
+int cycle_max_grid(int device, bool weighted) {
+  int sms = 0, n = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (weighted) {
+    cudaFuncSetAttribute(cycle_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_total<true>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<true>, Geo<true>::kThreads,
+                                                  smem_total<true>());
+  } else {
+    cudaFuncSetAttribute(cycle_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_total<false>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<false>, Geo<false>::kThreads,
+                                                  smem_total<false>());
+  }
+  return sms * (n > 0 ? 1 : 0);
+}
+
+cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,
+                         const CUtensorMap* tm_g, const CycleParams& prm, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(prm.grid);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (prm.weighted) {
+    cfg.blockDim = dim3(Geo<true>::kThreads);
+    cfg.dynamicSmemBytes = smem_total<true>();
+    return cudaLaunchKernelEx(&cfg, cycle_kernel<true>, *tm_e, *tm_code, *tm_g, prm);
+  }
+  cfg.blockDim = dim3(Geo<false>::kThreads);
+  cfg.dynamicSmemBytes = smem_total<false>();
+  return cudaLaunchKernelEx(&cfg, cycle_kernel<false>, *tm_e, *tm_code, *tm_g, prm);
+}
+
+}  // namespace gss

@@ -11,21 +11,18 @@ namespace gss {
 // ---------------------------------------------------------------------------
 // geometry (fixed at pack time: tile-blocked column pointers depend on it)
 // ---------------------------------------------------------------------------
-constexpr int kThreads = 256;              // consumer threads per CTA
-constexpr int kIpt = 8;                    // rows per consumer thread
-constexpr int kTileRows = kThreads * kIpt; // 2048 rows per tile
-constexpr int kProducerWarps = 1;
-constexpr int kCtaThreads = kThreads + 32 * kProducerWarps;
-constexpr int kGroup = 128;                // look-back group (tiles) with a published aggregate
-constexpr int kNnzCap = 256;               // per-stage smem capacity of a column's
-                                           // in-tile nonzero list (ints)
-constexpr int kStages = 4;
+constexpr int kIpt = 8;                     // rows per lane per pass
+constexpr int kTileRows = 2048;             // rows per tile (8 passes x 32 lanes x 8 rows)
+constexpr int kPasses = kTileRows / (32 * kIpt);
+constexpr int kNnzCap = 256;                // per-list smem capacity (ints) of a column's
+                                            // in-tile nonzero list
 
-// per-row code word (int32): built per engine from times/status/mask/strata
-constexpr uint32_t kCodeCount = 0x1FFFFFFFu;  // events in the tied block, at its last row
-constexpr uint32_t kCodeMasked = 1u << 29;    // row not visible to this engine
+// per-row code word (uint32): built per engine from times/status/mask/strata
+constexpr uint32_t kCodeCount = 0x0FFFFFFFu;  // events in the tied block, at its last row
+constexpr uint32_t kCodeCompeting = 1u << 28; // status==2 and visible (Fine-Gray u row)
+constexpr uint32_t kCodeMasked = 1u << 29;    // row not visible to this engine (or padding)
 constexpr uint32_t kCodeEvent = 1u << 30;     // status==1 and visible (for sum delta*eta)
-constexpr uint32_t kCodeSeg = 1u << 31;       // first row of a stratum (scan resets)
+constexpr uint32_t kCodeSeg = 1u << 31;       // first row of a stratum
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -64,6 +61,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(a),
       "r"(parity)
       : "memory");
+}
+
+// One non-blocking probe of a phase (for lane-divergent waits: the retry loop
+// stays visible to the compiler, so divergent lanes keep making progress).
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 // TMA 2D tile load (global -> shared), completion counted on `bar`.

@@ -1,5 +1,5 @@
-// gss_kernels.cuh — kernel parameter blocks shared by gss_kernels.cu and the
-// host side (gss_capi.cu).
+// gss_kernels.cuh — parameter blocks shared by the device code (gss_cycle.cu,
+// gss_aux.cu) and the host side of the C ABI (gss_capi.cu).
 #pragma once
 
 #include <cuda.h>
@@ -9,97 +9,114 @@
 namespace gss {
 
 // Per-engine device control block (zero-initialised at engine creation).
+// Written by CTA 0 of the cycle kernel at the end of a launch; read by every
+// CTA at launch start.
 struct Ctl {
-  // contended words each own a 128-byte line (atomics vs. polling)
-  alignas(128) unsigned int tile_counter;   // dynamic tile ids (phase C)
-  alignas(128) unsigned int ticket;         // CTA completion count (last CTA runs the tail)
-  alignas(128) unsigned int items_a;        // phase-A work items claimed
-  alignas(128) unsigned int groups_done;    // 32-tile groups scanned (last one scans groups)
-  alignas(128) unsigned long long ready;    // epoch whose tile prefixes are published
-  alignas(128) int tprev_valid;             // tsum holds fresh per-tile sums of the current e
-  int pad2;
-  unsigned long long epoch;    // launch generation tag for tile status words
-  // deferred state change applied by the NEXT sweep's tile phase
-  long long pend_col;          // -1: none
-  double pend_delta;
-  double pend_factor;          // exp(pend_delta), indicator cache rule
-  int refresh_pending;         // recompute eta/e from beta (refresh())
-  int halted;                  // an error stopped the cycle: later sweeps no-op
-  int err_code;                // gss_status of the first error in the cycle
-  int pad0;
-  long long err_col;
+  unsigned long long bar_base;         // grid-barrier counter value at launch start
   unsigned long long eta_absmax_bits;  // max |eta| at the last refresh/load (double bits)
-  unsigned long long absmax_next_bits; // max |eta| gathered by a refresh sweep in flight
   double bound_slack;                  // sum |delta| * max|x| of updates since then
-  long long accepted;          // Engine::accepted_ (engine.hpp:88)
-  long long refreshes;         // Engine::refreshes_
-  long long skipped;           // FitResult.skipped_steps (ccd.cpp:161-164)
-  // results of the last sweep
-  double grad_sum, hess_sum;   // GradHessSums
-  double gradient, hessian, fixed_term;
-  double ll_fixed, ll_logden, loglik;
-  int bad;                     // denominator <= 0 / NaN seen
+  long long accepted;                  // Engine::accepted_ (engine.hpp:88)
+  long long refreshes;                 // Engine::refreshes_
+  long long skipped;                   // FitResult.skipped_steps (ccd.cpp:161-164)
+  int rec_valid;                       // per-tile records serve a launch starting at rec_col
+  int pad0;
+  long long rec_col;
+  int err_code;                        // gss_status of the first error (0 = none)
   int pad1;
+  long long err_col;
+  // results of the last slot of each kind
+  double grad_sum, hess_sum, gradient, hessian, fixed_term;
+  double ll_fixed, ll_logden, loglik;
 };
 
-enum SweepMode : int { kModeGradApi = 0, kModeGradCcd = 1, kModeLoglik = 2 };
+// per-tile record (doubles) produced by the consumers of slot k for slot k+1:
+//   fwd lanes  : a = sum e, b = sum e*x, c = sum e*x^2            (x = next column)
+//   fwd s-parts: sums of the same over the rows of the slot-k column (the
+//                pending update of slot k+1), for the exp(delta) correction
+//   rev lanes  : the u-weighted versions (Fine-Gray)
+enum RecField : int {
+  kRa = 0, kRb, kRc, kRsa, kRsb, kRsc,
+  kRua, kRub, kRuc, kRusa, kRusb, kRusc,
+  kRecFields
+};
+constexpr int kRecStride = 12;
+// per-tile in-range carries (uncorrected + s-parts), written before the slot barrier
+//   0..5  : fwd segmented exclusive prefix inside the CTA range (a,b,c,sa,sb,sc)
+//   6     : 1 if a stratum starts at or before this tile inside the range (no CTA carry-in)
+//   8..13 : rev segmented inclusive suffix inside the CTA range (ua,ub,uc,usa,usb,usc)
+//   14    : 1 if a stratum starts after this tile inside the range (no CTA carry-in)
+constexpr int kCarStride = 16;
+// CTA payload exchanged at the slot barrier
+//   0..2 : slot partials (p0, p1, bad)
+//   3    : 1 if any tile of the range starts a stratum
+//   4..9 : fwd tail  (tiles from the last stratum-first tile): a,b,c,sa,sb,sc
+//   10..15: rev head (tiles before the first stratum-first tile): ua,ub,uc,usa,usb,usc
+//   16   : max |eta| (refresh), 17: overflow flag (exact validation)
+constexpr int kPayStride = 24;
 
-struct SweepParams {
-  // dataset (shared, read-only)
+enum SlotKind : int { kSlotGrad = 0, kSlotLoglik = 1 };
+enum LaunchMode : int { kModeApi = 0, kModeCcd = 1 };
+
+struct CycleParams {
+  // ---- dataset (shared, read-only) ----
   int64_t n, npad, p;
   int ntiles;
   int has_vals;
   const int64_t* col_ptr;
-  const int32_t* row_idx;      // padded by 4 ints
+  const int32_t* row_idx;      // padded device positions, +4 ints of slack
   const double* vals;          // parallel to row_idx (NULL => all 1.0)
   const uint8_t* col_ind;      // [p] indicator-column flags
   const uint32_t* tile_ptr;    // [p][ntiles+1] nnz offset of each tile start
-  const int64_t* row_ptr;      // CSR [n+1]
+  const int64_t* row_ptr;      // CSR [npad+1]
   const int32_t* csr_col;      // CSR [nnz] ascending per row
   const double* csr_val;       // CSR values (NULL => all 1.0)
   const double* colmax;        // [p] max |x| per column
-  // engine state
+  const uint8_t* tile_first;   // [ntiles] 1 if a stratum starts at the tile's first row
+  // ---- engine state ----
   double* eta;                 // [npad]
   double* e;                   // [npad] exp(eta) cache (0 for masked/pad rows)
-  const uint32_t* code;        // [npad]
-  const double* u;             // [npad] Fine-Gray IPCW u (NULL for cox)
-  const double* g;             // [npad] Fine-Gray IPCW g
+  const uint32_t* code;        // [npad] row code words
+  const double* g;             // [npad] Fine-Gray G(Y-) (NULL unless weighted)
   double* beta;                // [p]
   double* halfwidth;           // [p]
   const uint8_t* penalized;    // [p]
   const double* fixed;         // [p]
-  int pen_kind;
   int weighted;
+  int pen_kind;
   double pen_strength;
   long long recompute_interval;
-  // carry scratch
-  double* agg;                 // [ntiles][4] phase-A tile aggregates (f, a, b, c)
-  double* prefix;              // [ntiles][4] exclusive tile prefixes inside the 32-tile group
-  double* gsum;                // [ngroups][4] group totals
-  double* gpre;                // [ngroups][4] exclusive group prefixes
-  unsigned int* grp_cnt;       // [ngroups] phase-A tiles completed per group (reset by the tail)
-  double* tsum;                // [2][ntiles][2] fresh per-tile (f, sum e) by launch parity
-  const int32_t* tile_lastseg; // [ntiles] last stratum-start row in the tile, -1 if none
-  int has_mask;                // some rows are masked out (row_mask engine)
-  int has_strata;              // a stratum starts after row 0 (segmented scan needed)
-  double* tile_part;           // [ntiles][4]
+  // ---- launch ----
+  const int32_t* slot_col;     // [nslots] column of each slot, -1 = log-likelihood slot
+  int nslots;
+  int mode;                    // LaunchMode
+  int grid;                    // CTAs (<= co-resident capacity)
+  double* slot_out;            // optional [nslots][4] API results (gradient, hessian, fixed, ll)
+  // ---- scratch ----
+  double* trec;                // [ntiles][kRecStride]
+  double* tcar;                // [ntiles][kCarStride]
+  double* cpay;                // [2][grid][kPayStride]
+  unsigned int* bar;           // grid barrier counter
   Ctl* ctl;
-  int64_t column;              // scan column for grad modes
-  unsigned long long* trace;   // optional event trace [cap][2] (GSS_TRACE=1), else null
+  // optional event trace (GSS_TRACE=1): [cap][2] = (globaltimer ns, cta<<40|ev<<32|arg)
+  unsigned long long* trace;
   unsigned int* trace_n;
   unsigned int trace_cap;
+  int dbg;                     // debug/ablation bits (GSS_DEBUG): 1 skip tile work, 2 skip records,
+                               // 4 skip scans/transform
 };
 
-// launchers (gss_kernels.cu)
-cudaError_t launch_sweep(int mode, const CUtensorMap* tm_e, const CUtensorMap* tm_code,
-                         const SweepParams& prm, int grid, cudaStream_t s);
-int sweep_max_active_ctas_per_sm();
-int sweep_threads();
-size_t sweep_smem_bytes();
+// launchers (gss_cycle.cu)
+cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,
+                         const CUtensorMap* tm_g, const CycleParams& prm, cudaStream_t s);
+int cycle_max_grid(int device, bool weighted);
+size_t cycle_smem_bytes(bool weighted);
 
+// aux (gss_aux.cu)
 cudaError_t launch_validate_csc(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                 int64_t n, int* bad, cudaStream_t s);
 cudaError_t launch_exclusive_scan(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
+cudaError_t launch_remap_rows(int32_t* row_idx, int64_t nnz, const int64_t* dev_row,
+                              cudaStream_t s);
 cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s);
 cudaError_t launch_colmax(const int64_t* col_ptr, const double* vals, int64_t p,
@@ -116,13 +133,13 @@ cudaError_t launch_fixed_terms(const int64_t* col_ptr, const int32_t* row_idx,
                                const uint32_t* code, int64_t p, double* fixed,
                                cudaStream_t s);
 // load_beta: fresh eta = X beta into scratch, overflow flag; then commit
-cudaError_t launch_spmv_rows(const SweepParams& prm, const double* beta, double* eta_out,
+cudaError_t launch_spmv_rows(const CycleParams& prm, const double* beta, double* eta_out,
                              int* overflow, cudaStream_t s);
-cudaError_t launch_commit_eta(const SweepParams& prm, const double* eta_in, cudaStream_t s);
+cudaError_t launch_commit_eta(const CycleParams& prm, const double* eta_in, cudaStream_t s);
 // API update: check (validate-before-mutate) then commit
-cudaError_t launch_update_check(const SweepParams& prm, int64_t col, double delta, int* overflow,
+cudaError_t launch_update_check(const CycleParams& prm, int64_t col, double delta, int* overflow,
                                 cudaStream_t s);
-cudaError_t launch_update_commit(const SweepParams& prm, int64_t col, double delta,
+cudaError_t launch_update_commit(const CycleParams& prm, int64_t col, double delta,
                                  double factor, cudaStream_t s);
 
 }  // namespace gss

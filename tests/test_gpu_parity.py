@@ -26,7 +26,8 @@ def _sorted(c):
     return orc.assemble(*args, strata=strata)
 
 
-COX = [n for n in cases() if not n.startswith("ka_") and str(load(n)["model"]) == "cox"]
+GOLD = [n for n in cases() if not n.startswith("ka_")]
+COX = [n for n in GOLD if str(load(n)["model"]) == "cox"]
 
 
 @pytest.mark.parametrize("name", cases("ka_"))
@@ -40,11 +41,11 @@ def test_known_answers(capi, name):
     assert eng.log_likelihood() == pytest.approx(float(c["ll0"]), rel=1e-15, abs=1e-15)
 
 
-@pytest.mark.parametrize("name", COX)
+@pytest.mark.parametrize("name", GOLD)
 def test_derivatives_vs_reference(capi, name):
     c = load(name)
     ds = _sorted(c)
-    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), str(c["model"]))
     assert rel(eng.log_likelihood(), c["ll0"]) < TOL_DERIV
     eng.load_beta(c["beta_probe"])
     assert rel(eng.log_likelihood(), c["ll"]) < TOL_DERIV
@@ -54,14 +55,14 @@ def test_derivatives_vs_reference(capi, name):
         assert rel(gh["hessian"], c["hess"][j]) < TOL_DERIV, j
 
 
-@pytest.mark.parametrize("name", COX)
+@pytest.mark.parametrize("name", GOLD)
 def test_fits_vs_reference(capi, name):
     c = load(name)
     ds = _sorted(c)
     dd = capi.Dataset.from_sorted(ds)
     max_cycles = 200 if "strata" in c else 1000
     for k, pen, lam in fit_cases(c):
-        eng = capi.Engine(dd, "cox")
+        eng = capi.Engine(dd, str(c["model"]))
         r = eng.fit(penalty=pen, strength=lam, max_cycles=max_cycles)
         assert r["cycles"] == int(c[f"fit{k}_cycles"]), (pen, lam)
         assert np.max(rel(r["beta"], c[f"fit{k}_beta"])) < TOL_BETA, (pen, lam)
@@ -69,7 +70,7 @@ def test_fits_vs_reference(capi, name):
         assert np.max(rel(r["objective_trace"], c[f"fit{k}_trace"])) < TOL_DERIV
 
 
-def _random_sorted(n, p, density, seed, quant=None, strata=None, valued=False):
+def _random_sorted(n, p, density, seed, quant=None, strata=None, valued=False, competing=0.0):
     rng = np.random.default_rng(seed)
     nnz_per_col = rng.binomial(n, density, size=p)
     rows, cols, vals = [], [], []
@@ -86,6 +87,8 @@ def _random_sorted(n, p, density, seed, quant=None, strata=None, valued=False):
     if quant:
         t = np.ceil(t * quant) / quant
     status = (rng.random(n) < 0.7).astype(np.int64)
+    if competing:
+        status[(status == 0) & (rng.random(n) < competing)] = 2
     st = None if strata is None else rng.integers(0, strata, size=n)
     return orc.assemble(t, status, rows, cols, vals, p, strata=st)
 
@@ -175,3 +178,83 @@ def test_determinism(capi):
         eng.load_beta(np.array([0.2, -0.1, 0.3, 0.05]))
         outs.append([eng.grad_hessian(j)["gradient"] for j in range(4)] + [eng.log_likelihood()])
     assert outs[0] == outs[1] == outs[2]
+
+
+@pytest.mark.parametrize("n,p,quant,strata,valued", [
+    (90_000, 12, None, None, False),
+    (70_001, 10, 50.0, None, True),
+    (50_000, 8, 20.0, 5, False),
+])
+def test_finegray_multitile_vs_oracle(capi, n, p, quant, strata, valued):
+    """Forward-backward (u-weighted suffix) scan across many tiles and CTAs."""
+    ds = _random_sorted(n, p, 0.03, seed=7 * n + p, quant=quant, strata=strata, valued=valued,
+                        competing=0.6)
+    ref = orc.OracleEngine(ds, "finegray")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "finegray")
+    beta = np.random.default_rng(5).uniform(-0.3, 0.3, size=p)
+    ref.load_beta(beta)
+    eng.load_beta(beta)
+    assert rel(eng.log_likelihood(), ref.log_likelihood()) < TOL_DERIV
+    for j in range(p):
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        assert rel_cond(a["gradient"], b["gradient"], b["fixed_term"]) < TOL_DERIV, j
+        assert rel(a["hessian"], b["hessian"]) < TOL_DERIV, j
+    eng2 = capi.Engine(capi.Dataset.from_sorted(ds), "finegray")
+    ref2 = orc.OracleEngine(ds, "finegray")
+    r1 = eng2.fit(penalty="l1", strength=1.0, max_cycles=5)
+    r2 = ref2.fit(penalty="l1", strength=1.0, max_cycles=5)
+    assert r1["cycles"] == r2["cycles"]
+    assert np.max(rel(r1["beta"], r2["beta"])) < TOL_BETA
+    assert np.max(rel(r1["objective_trace"], r2["objective_trace"])) < TOL_DERIV
+
+
+def test_finegray_mask_equals_subset(capi):
+    ds = _random_sorted(40_000, 6, 0.05, seed=21, quant=30.0, competing=0.5)
+    mask = (np.random.default_rng(2).random(ds.n) < 0.75).astype(np.uint8)
+    keep = np.nonzero(mask)[0]
+    sub_cols = np.repeat(np.arange(ds.p), np.diff(ds.col_ptr))
+    remap = -np.ones(ds.n, np.int64)
+    remap[keep] = np.arange(len(keep))
+    sel = remap[ds.row_idx] >= 0
+    sub = orc.assemble(ds.times[keep], ds.status[keep], remap[ds.row_idx[sel]], sub_cols[sel],
+                       ds.vals[sel], ds.p)
+    ref = orc.OracleEngine(sub, "finegray")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "finegray", row_mask=mask)
+    beta = np.linspace(-0.2, 0.3, ds.p)
+    ref.load_beta(beta)
+    eng.load_beta(beta)
+    assert rel(eng.log_likelihood(), ref.log_likelihood()) < TOL_DERIV
+    for j in range(ds.p):
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        assert rel_cond(a["gradient"], b["gradient"], b["fixed_term"]) < TOL_DERIV
+        assert rel(a["hessian"], b["hessian"]) < TOL_DERIV
+
+
+def test_finegray_without_competing_is_cox(capi):
+    """tests/test_engine.cpp:293-310: no status-2 rows => the Cox computation."""
+    ds = _random_sorted(30_000, 5, 0.04, seed=3, quant=40.0)
+    dd = capi.Dataset.from_sorted(ds)
+    a, b = capi.Engine(dd, "cox"), capi.Engine(dd, "finegray")
+    beta = np.array([0.1, -0.2, 0.05, 0.3, -0.1])
+    a.load_beta(beta)
+    b.load_beta(beta)
+    for j in range(ds.p):
+        assert a.grad_hessian(j) == b.grad_hessian(j)
+    assert a.log_likelihood() == b.log_likelihood()
+    ra = capi.Engine(dd, "cox").fit(penalty="l1", strength=1.0, max_cycles=4)
+    rb = capi.Engine(dd, "finegray").fit(penalty="l1", strength=1.0, max_cycles=4)
+    assert np.array_equal(ra["beta"], rb["beta"])
+
+
+@pytest.mark.parametrize("model", ["cox", "finegray"])
+def test_grad_hessian_all_matches_single(capi, model):
+    ds = _random_sorted(60_000, 9, 0.03, seed=17, quant=25.0, competing=0.5 if model == "finegray" else 0.0)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), model)
+    eng.load_beta(np.linspace(-0.2, 0.2, ds.p))
+    allg = eng.grad_hessian_all()
+    for j in range(ds.p):
+        gh = eng.grad_hessian(j)
+        # same kernel, but the batched launch builds each carry from the previous
+        # slot's per-tile records (another fixed summation order)
+        assert rel_cond(allg["gradient"][j], gh["gradient"], gh["fixed_term"]) < 1e-13
+        assert rel(allg["hessian"][j], gh["hessian"]) < 1e-13

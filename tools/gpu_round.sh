@@ -4,7 +4,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv | tail -1
 for step in "$@"; do
 case $step in
 tests) timeout 900 python -m pytest tests -x -q -m gpu --timeout 300 2>&1 | tail -8 ;;
-trace) timeout 300 python tools/trace_sweep.py --n 10000000 --p 16 2>&1 | tail -16 ;;
+trace) echo "trace: removed with the per-coordinate sweep";;
 fit) timeout 300 python tools/prof_sweep.py --n 10000000 --p 64 --mode fit --cycles 3 2>&1 | tail -3 ;;
 api) timeout 300 python tools/prof_sweep.py --n 10000000 --p 64 --mode api --reps 50 2>&1 | tail -2 ;;
 launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 70 -c 140 --csv \
