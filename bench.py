@@ -8,11 +8,12 @@ Synthetic data from the device generator (gss_sim.h): simulate_cox design
 family (src/simgen.cpp:108-122) with administrative censoring at the 0.9
 quantile and times quantised to 1e-3.
 
-A "step" is one CCD cycle: p fused coordinate kernels (deferred sparse
-update + decoupled-look-back scan/transform/reduce + coordinate step) plus
-the objective kernel, replayed as one CUDA graph.  Warm-up steps are the
-first W cycles of the fit, the K timed steps the next K cycles, each timed
-with CUDA events on the engine stream.  Per-cycle working set (~2.5 GB of
+A "step" is one CCD cycle: ONE launch of the persistent cycle kernel
+(gss_cycle.cu) that walks the p coordinates (deferred sparse update + fused
+risk-set scan/transform/reduce + coordinate step, one grid-wide exchange per
+coordinate) and then evaluates the objective.  Warm-up steps are the first W
+cycles of the fit, the K timed steps the next K cycles, each timed with CUDA
+events on the engine stream.  Per-cycle working set (~2.5 GB of
 CSC indices + 120 MB of per-row state) is far larger than L2.
 
   value : coordinate updates / s, device-resident inputs (whole job, all ranks)
@@ -271,7 +272,7 @@ def roofline(n, col_ptr, cycles_ms, accepted_per_cycle, p, launches_per_cycle):
             "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if os.path.exists(PEAKS)
             else "fallback (B200_PROFILING.md 6.65 TB/s)",
             "algorithmic_bytes_per_coordinate": round(12.0 * n + 4.0 * avg_nnz, 1),
-            "kernel": "sweep_kernel<kModeGradCcd> (+1 objective sweep per cycle)"}
+            "kernel": "cycle_kernel<false> (p coordinate slots + 1 objective slot per launch)"}
 
 
 def run_gss(args, dist):
@@ -334,7 +335,7 @@ def run_gss(args, dist):
             "n": args.n, "p": args.p, "density": args.density, "nnz": int(sim.nnz),
             "penalty": "l1", "strength": args.strength, "time_quantum": args.quantum,
             "censoring_quantile": args.censoring_quantile,
-            "step": "one CCD cycle (p fused coordinate kernels + objective) as a CUDA graph",
+            "step": "one CCD cycle = one persistent cycle-kernel launch (p coordinates + objective)",
             "l2": "inputs larger than L2: per-cycle working set ~2.5 GB (no flush needed)",
             "parallelism": f"replicas{dist.world}",
         },
@@ -346,7 +347,7 @@ def run_gss(args, dist):
                 "path": "gss_dataset_pack + gss_engine_create + gss_engine_fit (tol 1e-6) from "
                         "pinned host buffers"},
         "roofline": roof,
-        "gpu_launches": int(K * (args.p + 1)),
+        "gpu_launches": int(K),
         "clocks": clocks,
         "fit_objective_after_timed_cycles": res["objective"],
     }
