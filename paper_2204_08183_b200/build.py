@@ -49,25 +49,39 @@ def ext_path():
     return os.path.join(PKG, "_survscan" + sysconfig.get_config_var("EXT_SUFFIX"))
 
 
-def build_pymodule(force=False):
+LIBSURVSCAN = os.path.join(PKG, "libsurvscan_b200.so")
+
+
+def build_libsurvscan(force=False):
+    """C++ mirror of the reference API (namespace survscan) over libgss."""
     host = os.path.join(CSRC, "host")
-    srcs = sorted(glob.glob(os.path.join(host, "*.cpp")))
-    if not srcs:
-        return None
+    srcs = sorted(s for s in glob.glob(os.path.join(host, "*.cpp"))
+                  if not s.endswith("bindings.cpp"))
     deps = srcs + glob.glob(os.path.join(host, "survscan", "*.hpp")) + [LIBGSS]
+    if force or _newer(LIBSURVSCAN, deps):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-pthread",
+              "-I" + host, *srcs, "-L" + PKG, "-lgss", "-Wl,-rpath,$ORIGIN",
+              "-o", LIBSURVSCAN])
+    return LIBSURVSCAN
+
+
+def build_pymodule(force=False):
+    """pybind11 `_survscan`: the reference's Python API over libsurvscan_b200."""
+    host = os.path.join(CSRC, "host")
+    src = os.path.join(host, "bindings.cpp")
+    deps = [src, LIBSURVSCAN] + glob.glob(os.path.join(host, "survscan", "*.hpp"))
     out = ext_path()
     if force or _newer(out, deps):
         import pybind11
-        cuda_inc = "/usr/local/cuda/include"
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
-              "-I" + host, "-I" + os.path.join(ROOT, "include"), "-I" + cuda_inc,
-              "-I" + sysconfig.get_paths()["include"], "-I" + pybind11.get_include(),
-              *srcs, "-L" + PKG, "-lgss", "-Wl,-rpath,$ORIGIN", "-o", out])
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-pthread",
+              "-I" + host, "-I" + sysconfig.get_paths()["include"], "-I" + pybind11.get_include(),
+              src, "-L" + PKG, "-lsurvscan_b200", "-lgss", "-Wl,-rpath,$ORIGIN", "-o", out])
     return out
 
 
 def build(force=False):
     build_libgss(force)
+    build_libsurvscan(force)
     build_pymodule(force)
 
 

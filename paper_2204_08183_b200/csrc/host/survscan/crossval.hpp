@@ -1,0 +1,64 @@
+// survscan/crossval.hpp — model selection with the reference API
+// (/root/reference/proj/include/survscan/crossval.hpp:13-76).  Folds are row
+// masks on the device-resident dataset (no subset copies); (grid, replicate)
+// tasks are spread over the visible GPUs by the same slot-per-task merge, so
+// the device count never changes the result.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "survscan/ccd.hpp"
+
+namespace survscan {
+
+struct CVConfig {
+  std::uint32_t folds = 10;
+  std::uint32_t repetitions = 10;
+  std::vector<double> grid;
+  std::uint64_t seed = 0;
+  std::uint32_t parallel_replicates = 1;  // worker threads per device
+  void validate() const;
+};
+
+struct CVPoint {
+  double strength = 0.0;
+  double mean_loglik = 0.0;
+  double spread = 0.0;
+  std::uint32_t evaluations = 0;
+};
+
+struct CVResult {
+  std::vector<CVPoint> points;
+  double selected_value = 0.0;
+  FitResult final_fit;
+  std::uint32_t failed_replicates = 0;
+};
+
+std::uint64_t mix64(std::uint64_t x);
+std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t a, std::uint64_t b = 0);
+
+std::vector<std::uint32_t> fold_assignment(std::size_t n, std::uint32_t folds,
+                                           std::uint64_t seed, std::uint64_t grid_index,
+                                           std::uint64_t replicate);
+double held_out_loglik(const SurvivalDataset& ds, const std::vector<std::uint32_t>& fold_of,
+                       std::uint32_t fold, Model model, const std::vector<double>& beta,
+                       const ChunkPlan& plan = {});
+double gamma_max(const SurvivalDataset& ds, Model model, const ChunkPlan& plan = {});
+std::vector<double> auto_grid(double top);
+// devices: GPUs to spread the tasks over (empty = all visible)
+CVResult cross_validate(const SurvivalDataset& ds, Model model, PenaltyKind kind,
+                        const CVConfig& cv, const FitConfig& fit_config = {},
+                        const std::vector<int>& devices = {});
+
+struct BootstrapInterval {
+  double lower = 0.0;
+  double upper = 0.0;
+  std::uint32_t failed_resamples = 0;
+};
+BootstrapInterval bootstrap_interval(const SurvivalDataset& ds, Model model,
+                                     const PenaltySpec& penalty, const FitConfig& fit_config,
+                                     std::size_t coefficient_index, std::uint32_t resamples,
+                                     std::uint64_t seed);
+
+}  // namespace survscan

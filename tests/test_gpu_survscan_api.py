@@ -1,0 +1,165 @@
+"""The drop-in Python API (`survscan`, the reference's bindings surface,
+bindings/survscan_py.cpp:105-326) on the device engine, plus parity of the
+C++ drivers (fit, cross_validate, gamma_max) against the UNMODIFIED reference
+module built in oracle/_ref (test infrastructure, run on the host CPU)."""
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from tests._common import TOL_BETA, TOL_DERIV, load, raw, rel
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ss():
+    import survscan
+    assert survscan.device_count() > 0
+    return survscan
+
+
+@pytest.fixture(scope="module")
+def ref():
+    d = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(d):
+        pytest.skip("reference module not built (oracle/build_ref.sh)")
+    sys.path.insert(0, d)
+    try:
+        import _survscan as r
+    except ImportError as exc:
+        pytest.skip(f"reference module unavailable: {exc}")
+    return r
+
+
+@pytest.fixture(scope="module")
+def fg(ss):
+    return ss.simulate_finegray(n=400, p=6, density=0.2, seed=5, censoring_quantile=0.9)
+
+
+def test_simulation_shape_and_determinism(ss, fg):
+    ds, b1, b2 = fg
+    assert ds.n == 400 and ds.p == 6 and ds.has_competing
+    assert np.array_equal(b2, -b1)
+    again, c1, _ = ss.simulate_finegray(n=400, p=6, density=0.2, seed=5, censoring_quantile=0.9)
+    assert again.content_hash == ds.content_hash and np.array_equal(b1, c1)
+    assert set(np.unique(ds.status)) <= {0, 1, 2}
+
+
+def test_fit_monotone_and_finegray_reduces_to_cox(ss, fg):
+    ds = fg[0]
+    res = ss.fit(ds, model="finegray", penalty="l1", strength=0.05)
+    assert res["converged"] and res["beta"].shape == (6,)
+    tr = res["objective_trace"]
+    assert all(b >= a - 1e-10 for a, b in zip(tr, tr[1:]))
+    cox_ds, _ = ss.simulate_cox(n=300, p=4, density=0.2, seed=9, censoring_quantile=0.85)
+    a = ss.fit(cox_ds, model="cox")
+    b = ss.fit(cox_ds, model="finegray")
+    assert np.max(np.abs(a["beta"] - b["beta"])) <= 1e-12
+
+
+def test_loglik_gradient_finite_difference(ss, fg):
+    ds = fg[0]
+    beta = np.full(ds.p, 0.01)
+    base = ss.log_likelihood(ds, "finegray", beta)
+    assert math.isfinite(base) and base < 0
+    h = 1e-5
+    up, dn = beta.copy(), beta.copy()
+    up[2] += h
+    dn[2] -= h
+    fd = (ss.log_likelihood(ds, "finegray", up) - ss.log_likelihood(ds, "finegray", dn)) / (2 * h)
+    g, hess = ss.grad_hessian(ds, "finegray", beta, 2)
+    assert hess <= 0 and abs(fd - g) <= 1e-6 * max(1.0, abs(g))
+
+
+def test_cross_validate_gamma_max(ss, fg):
+    ds = fg[0]
+    cv = ss.cross_validate(ds, model="finegray", penalty="l1", folds=3, repetitions=1, seed=4)
+    strengths = [pt["strength"] for pt in cv["curve"]]
+    assert len(strengths) == 10 and strengths == sorted(strengths)
+    assert cv["selected"] in strengths
+    top = ss.gamma_max(ds, model="finegray")
+    assert strengths[-1] == top and ss.auto_grid(top)[0] == top / 1000.0
+    assert ss.fit(ds, model="finegray", penalty="l1", strength=top)["nonzero_count"] == 0
+
+
+def test_bootstrap_interval(ss, fg):
+    lo, hi, failed = ss.bootstrap_interval(fg[0], model="finegray", penalty="l1", strength=0.05,
+                                           coefficient=1, resamples=100, seed=3)
+    assert lo <= hi and failed == 0
+
+
+def test_errors_surface(ss, fg):
+    with pytest.raises(ss.SurvscanError):
+        ss.fit(fg[0], model="cox")  # competing rows under a cox model
+    with pytest.raises(ss.SurvscanError):
+        ss.grad_hessian(fg[0], "finegray", np.zeros(6), 17)
+
+
+def _both(ss, ref, name):
+    c = load(name)
+    (t, s, rows, cols, vals, p), _ = raw(c)
+    a = ss.dataset_from_coo(t, s, rows, cols, vals, p)
+    b = ref.dataset_from_coo(t, s, rows, cols, vals, p)
+    return str(c["model"]), a, b
+
+
+@pytest.mark.parametrize("name", ["cox_small", "cox_ties", "cox_valued", "fg_small", "fg_ties"])
+def test_fit_parity_with_reference_module(ss, ref, name):
+    model, a, b = _both(ss, ref, name)
+    for pen, lam in [("none", 0.0), ("l1", 0.5), ("l2", 2.0)]:
+        ra = ss.fit(a, model=model, penalty=pen, strength=lam, tol=1e-12, max_cycles=400)
+        rb = ref.fit(b, model=model, penalty=pen, strength=lam, tol=1e-12, max_cycles=400,
+                     threads=1)
+        assert ra["cycles"] == rb["cycles"], (pen, lam)
+        assert np.max(rel(ra["beta"], rb["beta"])) < TOL_BETA
+        assert rel(ra["objective"], rb["objective"]) < TOL_DERIV
+        assert ra["nonzero_count"] == rb["nonzero_count"]
+
+
+@pytest.mark.parametrize("name", ["cox_small", "fg_small"])
+def test_gamma_max_and_loglik_parity(ss, ref, name):
+    model, a, b = _both(ss, ref, name)
+    assert rel(ss.gamma_max(a, model=model), ref.gamma_max(b, model=model)) < TOL_DERIV
+    beta = np.linspace(-0.2, 0.2, a.p)
+    assert rel(ss.log_likelihood(a, model, beta), ref.log_likelihood(b, model, beta)) < TOL_DERIV
+
+
+@pytest.mark.parametrize("name,model", [("cox_ties", "cox"), ("fg_small", "finegray")])
+def test_cross_validate_parity_with_reference_module(ss, ref, name, model):
+    """Same seeded partitions (counter-seeded shuffles), device row-mask folds
+    vs the reference's subset copies: identical curves."""
+    _, a, b = _both(ss, ref, name)
+    grid = list(np.geomspace(0.05, 5.0, 5))
+    kw = dict(model=model, penalty="l1", grid=grid, folds=3, repetitions=2, seed=11, tol=1e-12,
+              max_cycles=400)
+    ca = ss.cross_validate(a, **kw)
+    cb = ref.cross_validate(b, threads=1, **kw)
+    assert ca["selected"] == cb["selected"]
+    assert ca["failed_replicates"] == cb["failed_replicates"]
+    for pa, pb in zip(ca["curve"], cb["curve"]):
+        assert pa["evaluations"] == pb["evaluations"]
+        assert rel(pa["mean_loglik"], pb["mean_loglik"]) < 1e-9
+    assert np.max(rel(ca["final_fit"]["beta"], cb["final_fit"]["beta"])) < TOL_BETA
+
+
+def test_engine_class_surface(ss):
+    c = load("cox_small")
+    (t, s, rows, cols, vals, p), _ = raw(c)
+    ds = ss.dataset_from_coo(t, s, rows, cols, vals, p)
+    eng = ss.Engine(ds, "cox", recompute_interval=3)
+    eng.load_beta(c["beta_probe"])
+    assert rel(eng.log_likelihood(), c["ll"]) < TOL_DERIV
+    for j in range(p):
+        g, h, f = eng.grad_hessian(j)
+        assert rel(h, c["hess"][j]) < TOL_DERIV
+    eng.load_beta(np.zeros(p))
+    for j, d in [(0, 0.1), (1, -0.2), (2, 0.3)]:
+        eng.update_xbeta_sparse(j, d)
+    assert eng.accepted_updates == 3 and eng.refresh_count == 1
+    r = eng.fit(penalty="l1", strength=0.5)
+    assert rel(r["objective"], float(c["fit1_objective"])) < TOL_DERIV
