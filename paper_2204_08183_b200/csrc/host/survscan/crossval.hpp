@@ -46,6 +46,26 @@ double held_out_loglik(const SurvivalDataset& ds, const std::vector<std::uint32_
                        const ChunkPlan& plan = {});
 double gamma_max(const SurvivalDataset& ds, Model model, const ChunkPlan& plan = {});
 std::vector<double> auto_grid(double top);
+// Pieces of cross_validate for multi-process drivers (one process per GPU):
+// the resolved grid, the event-free-fold precheck, the per-task fold scores
+// (task = grid_index * repetitions + replicate; failed => empty), and the
+// task-ordered merge + final refit.
+struct TaskScores {
+  std::vector<double> fold_loglik;
+  bool failed = false;
+};
+std::vector<double> cv_grid(const SurvivalDataset& ds, Model model, const CVConfig& cv,
+                            const FitConfig& fit_config);
+void cv_check_folds(const SurvivalDataset& ds, const CVConfig& cv, std::size_t n_grid);
+std::vector<TaskScores> cv_run_tasks(const SurvivalDataset& ds, Model model, PenaltyKind kind,
+                                     const std::vector<double>& grid, const CVConfig& cv,
+                                     const FitConfig& fit_config,
+                                     const std::vector<std::size_t>& tasks,
+                                     const std::vector<int>& devices = {});
+CVResult cv_merge(const SurvivalDataset& ds, Model model, PenaltyKind kind,
+                  const std::vector<double>& grid, const CVConfig& cv, const FitConfig& fit_config,
+                  const std::vector<TaskScores>& all_tasks, bool refit = true);
+
 // devices: GPUs to spread the tasks over (empty = all visible)
 CVResult cross_validate(const SurvivalDataset& ds, Model model, PenaltyKind kind,
                         const CVConfig& cv, const FitConfig& fit_config = {},

@@ -163,3 +163,20 @@ def test_engine_class_surface(ss):
     assert eng.accepted_updates == 3 and eng.refresh_count == 1
     r = eng.fit(penalty="l1", strength=0.5)
     assert rel(r["objective"], float(c["fit1_objective"])) < TOL_DERIV
+
+
+def test_distributed_driver_single_rank_equals_cross_validate(ss):
+    """C4 driver (one process per GPU) at world size 1 == the C++ cross_validate."""
+    from paper_2204_08183_b200.distributed import cross_validate_distributed
+    c = load("cox_ties")
+    (t, s, rows, cols, vals, p), _ = raw(c)
+    ds = ss.dataset_from_coo(t, s, rows, cols, vals, p)
+    grid = [0.05, 0.4, 3.0]
+    kw = dict(model="cox", penalty="l1", grid=grid, folds=3, repetitions=2, seed=5, tol=1e-10,
+              max_cycles=300)
+    a = cross_validate_distributed(ds, **kw)
+    b = ss.cross_validate(ds, **kw)
+    assert a["selected"] == b["selected"]
+    for pa, pb in zip(a["curve"], b["curve"]):
+        assert pa["mean_loglik"] == pb["mean_loglik"] and pa["evaluations"] == pb["evaluations"]
+    assert np.array_equal(a["final_fit"]["beta"], b["final_fit"]["beta"])
