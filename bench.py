@@ -45,7 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_cycle_summary.json")
 
 
 def parse():

@@ -171,6 +171,26 @@ int gss_engine_grad_hessian_all(gss_engine* e, double* gradient, double* hessian
  */
 int gss_engine_max_abs_gradient(gss_engine* e, double* out);
 
+/*
+ * Patient sharding (config C5): an engine over one contiguous row shard of the
+ * global order (cut at tied-block boundaries; stratum_start[0] = 0 marks a
+ * shard whose first row continues a stratum).  Per coordinate every rank
+ *   1. gss_shard_aggregate(e, j, agg)  -> agg[0] stratum-start flag,
+ *      agg[1..3] fwd tail (sum e, e*x_j, e*x_j^2 from the last stratum start),
+ *      agg[4..6] rev head (Fine-Gray u-weighted), agg[7] first row starts a stratum;
+ *   2. all-gathers the aggregates and composes its carry (segmented prefix of
+ *      the earlier shards' tails / suffix of the later shards' heads);
+ *   3. gss_shard_sums(e, j, carry, &s0, &s1) -> this shard's (grad_sum,
+ *      hess_sum) of fused_grad_hess (scan_kernels.hpp:74-214), or for j = -1
+ *      (sum delta*eta, sum d*log D) of the log-likelihood;
+ *   4. all-reduces the sums in rank order, finishes and steps identically.
+ * carry8: [0..2] fwd (a, b, c), [4..6] rev (ua, ub, uc), others 0.
+ */
+int gss_shard_aggregate(gss_engine* e, int64_t column, double* agg8);
+int gss_shard_sums(gss_engine* e, int64_t column, const double* carry8, double* s0, double* s1);
+/* validate-before-mutate of update_xbeta_sparse (src/engine.cpp:171-190) without mutating */
+int gss_engine_update_validate(gss_engine* e, int64_t column, double delta, int32_t* overflow);
+
 /* Device time (ms) of the last fit's coordinate cycles, for bench. */
 int gss_engine_last_timing(gss_engine* e, double* scan_ms, int64_t* launches);
 /* Per-cycle statistics of the last fit: CUDA-event device time of each

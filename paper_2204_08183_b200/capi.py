@@ -29,7 +29,8 @@ EXPORTS = [
     "gss_engine_get_xbeta", "gss_engine_get_exp_xbeta", "gss_engine_get_fixed_terms",
     "gss_engine_get_ipcw", "gss_engine_counters", "gss_engine_fit",
     "gss_engine_max_abs_gradient", "gss_engine_last_timing", "gss_engine_grad_hessian_all",
-    "gss_engine_cycle_stats",
+    "gss_engine_cycle_stats", "gss_shard_aggregate", "gss_shard_sums",
+    "gss_engine_update_validate",
 ]
 
 
@@ -245,6 +246,25 @@ class Engine:
         g, h, f = np.empty(self.ds.p), np.empty(self.ds.p), np.empty(self.ds.p)
         check(lib().gss_engine_grad_hessian_all(self.h, _p(g), _p(h), _p(f)))
         return {"gradient": g, "hessian": h, "fixed_term": f}
+
+    # ---- patient sharding (config C5) ----
+    def shard_aggregate(self, column):
+        out = np.zeros(8)
+        check(lib().gss_shard_aggregate(self.h, ctypes.c_int64(column), _p(out)))
+        return out
+
+    def shard_sums(self, column, carry):
+        c = np.ascontiguousarray(carry, np.float64)
+        s0, s1 = ctypes.c_double(), ctypes.c_double()
+        check(lib().gss_shard_sums(self.h, ctypes.c_int64(column), _p(c), ctypes.byref(s0),
+                                   ctypes.byref(s1)))
+        return s0.value, s1.value
+
+    def update_validate(self, column, delta):
+        over = ctypes.c_int32()
+        check(lib().gss_engine_update_validate(self.h, ctypes.c_int64(column),
+                                               ctypes.c_double(delta), ctypes.byref(over)))
+        return bool(over.value)
 
     def max_abs_gradient(self):
         out = ctypes.c_double()

@@ -146,6 +146,7 @@ struct gss_engine {
   double *beta = nullptr, *halfwidth = nullptr, *fixed = nullptr;
   uint8_t* penalized = nullptr;
   double *trec = nullptr, *tcar = nullptr, *cpay = nullptr, *slot_out = nullptr;
+  double *ext = nullptr, *shard = nullptr;  // patient-shard carry in / aggregate out
   int32_t* slot_col = nullptr;
   unsigned int* bar = nullptr;
   Ctl* ctl = nullptr;
@@ -165,7 +166,7 @@ struct gss_engine {
     for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
                     (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
                     (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
-                    (void*)dflag})
+                    (void*)dflag, (void*)ext, (void*)shard})
       if (q) cudaFree(q);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (ev0) cudaEventDestroy(ev0);
@@ -313,8 +314,10 @@ int check_engine(gss_engine* E) {
   return GSS_OK;
 }
 
-// One launch of the cycle kernel over `slots` (API or CCD mode).
-int run_slots(gss_engine* E, const std::vector<int32_t>& slots, int mode, bool want_out) {
+// One launch of the cycle kernel over `slots` (API or CCD mode).  Shard
+// options: ext = apply the external carry, prologue = records + shard aggregate only.
+int run_slots(gss_engine* E, const std::vector<int32_t>& slots, int mode, bool want_out,
+              bool ext = false, bool prologue = false) {
   if (slots.empty()) return GSS_OK;
   if (static_cast<int64_t>(slots.size()) > E->ds->p + 1)
     return fail(GSS_ERR_DOMAIN, "too many slots");
@@ -325,6 +328,11 @@ int run_slots(gss_engine* E, const std::vector<int32_t>& slots, int mode, bool w
   P.nslots = static_cast<int>(slots.size());
   P.mode = mode;
   P.slot_out = want_out ? E->slot_out : nullptr;
+  P.ext = ext ? E->ext : nullptr;
+  P.shard_out = prologue ? E->shard : nullptr;
+  P.prologue_only = prologue ? 1 : 0;
+  P.reuse_records = ext ? 1 : 0;
+  if (prologue) P.nslots = 0;  // nothing is streamed
   GSS_CUDA(launch_cycle(&E->tm_e, &E->tm_code, &E->tm_g, P, E->stream));
   return GSS_OK;
 }
@@ -412,9 +420,11 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     ds->npad = npad;
     ds->ntiles = static_cast<int>(npad / kTileRows);
     ds->h_tile_first.assign(static_cast<size_t>(ds->ntiles), 0);
-    ds->h_tile_first[0] = 1;
-    for (int64_t i = 0; i < n; ++i)
-      if (i == 0 || ds->stratum_of[i] != ds->stratum_of[i - 1])
+    // row 0 starts a stratum unless the caller marks it as continuing one from
+    // a previous patient shard (stratum_start[0] == 0)
+    ds->h_tile_first[0] = (h->stratum_start && n > 0) ? (h->stratum_start[0] ? 1 : 0) : 1;
+    for (int64_t i = 1; i < n; ++i)
+      if (ds->stratum_of[i] != ds->stratum_of[i - 1])
         ds->h_tile_first[ds->dev_row[i] / kTileRows] = 1;
   }
   ds->h_col_ptr.assign(h->col_ptr, h->col_ptr + p + 1);
@@ -593,6 +603,9 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(dalloc(&E->bar, 1));
   EK(dalloc(&E->ctl, 1));
   EK(dalloc(&E->dflag, 4));
+  EK(dalloc(&E->ext, 8));
+  EK(dalloc(&E->shard, 8));
+  EK(cudaMemsetAsync(E->ext, 0, 8 * sizeof(double), E->stream));
   if (E->weighted) EK(dalloc(&E->g, npad));
   EK(cudaMallocHost(reinterpret_cast<void**>(&E->h_ctl), sizeof(Ctl)));
   std::memset(E->h_ctl, 0, sizeof(Ctl));
@@ -980,6 +993,54 @@ int gss_engine_max_abs_gradient(gss_engine* E, double* out) {
   double top = 0.0;
   for (double v : g) top = std::max(top, std::abs(v));
   *out = top;
+  return GSS_OK;
+}
+
+// ---- patient sharding (config C5): see include/gss.h ----------------------
+int gss_shard_aggregate(gss_engine* E, int64_t column, double* out8) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < -1 || column >= E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "shard: bad column");
+  rc = run_slots(E, {static_cast<int32_t>(column)}, kModeApi, false, false, true);
+  if (rc) return rc;
+  GSS_CUDA(cudaMemcpyAsync(out8, E->shard, 8 * sizeof(double), cudaMemcpyDeviceToHost, E->stream));
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (E->h_ctl->err_code) return device_error(E, "shard aggregate");
+  return GSS_OK;
+}
+
+int gss_shard_sums(gss_engine* E, int64_t column, const double* carry8, double* s0, double* s1) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < -1 || column >= E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "shard: bad column");
+  GSS_CUDA(cudaMemcpyAsync(E->ext, carry8, 8 * sizeof(double), cudaMemcpyHostToDevice, E->stream));
+  rc = run_slots(E, {static_cast<int32_t>(column)}, kModeApi, false, true, false);
+  if (rc) return rc;
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  if (E->h_ctl->err_code) return device_error(E, "shard sums");
+  if (column >= 0) {
+    *s0 = E->h_ctl->grad_sum;
+    *s1 = E->h_ctl->hess_sum;
+  } else {
+    *s0 = E->h_ctl->ll_fixed;
+    *s1 = E->h_ctl->ll_logden;
+  }
+  return GSS_OK;
+}
+
+int gss_engine_update_validate(gss_engine* E, int64_t column, double delta, int32_t* overflow) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < 0 || column >= E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "validate: bad column");
+  cudaStream_t s = E->stream;
+  GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
+  GSS_CUDA(launch_update_check(E->prm, column, delta, E->dflag, s));
+  int over = 0;
+  GSS_CUDA(cudaMemcpyAsync(&over, E->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  *overflow = over;
   return GSS_OK;
 }
 

@@ -119,6 +119,7 @@ struct Tail {
   int flag;
   int need_exact, refresh, valued;
   int cstar, cend;
+  int ext_f, ext_r;
 };
 
 template <bool FG>
@@ -1289,13 +1290,62 @@ __device__ __noinline__ void gather_payloads(const CycleParams& P, const double*
 
 // corrected CTA carries from the gathered sums (thread 0)
 template <bool FG>
-__device__ __forceinline__ void set_carry_in(Tail<FG>* tl, double k1) {
+__device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl, double k1) {
 #pragma unroll
-  for (int i = 0; i < 3; ++i) tl->ss.cin_f[i] = __dadd_rn(tl->gs[3 + i], __dmul_rn(k1, tl->gs[6 + i]));
+  for (int i = 0; i < 3; ++i) {
+    double v = __dadd_rn(tl->gs[3 + i], __dmul_rn(k1, tl->gs[6 + i]));
+    if (tl->ext_f) v = __dadd_rn(__ldcg(P.ext + i), v);  // shards before this one
+    tl->ss.cin_f[i] = v;
+  }
   if constexpr (FG) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
-      tl->ss.cin_r[i] = __dadd_rn(tl->gs[9 + i], __dmul_rn(k1, tl->gs[12 + i]));
+    for (int i = 0; i < 3; ++i) {
+      double v = __dadd_rn(tl->gs[9 + i], __dmul_rn(k1, tl->gs[12 + i]));
+      if (tl->ext_r) v = __dadd_rn(v, __ldcg(P.ext + 4 + i));  // shards after this one
+      tl->ss.cin_r[i] = v;
+    }
+  }
+}
+
+// This shard's aggregate from the CTA payloads (warp 0 of CTA 0; fixed order):
+// fwd tail = tails of CTAs from the last stratum-start CTA on, rev head =
+// heads of CTAs up to the first stratum-start CTA (carry sums of other shards
+// are composed by the host, segmented over shards).
+template <bool FG>
+__device__ void shard_aggregate(const CycleParams& P, const double* pall, const Tail<FG>* tl,
+                                int lane) {
+  const int G = P.grid;
+  int last = -1, first = G;
+  for (int c = 0; c < G; ++c)
+    if (tl->cflag[c]) {
+      if (last < c) last = c;
+      if (first > c) first = c;
+    }
+  double f[3] = {0, 0, 0}, r[3] = {0, 0, 0};
+  for (int c = lane; c < G; c += 32) {
+    const double* py = pall + size_t(c) * kPayStride;
+    if (c >= (last < 0 ? 0 : last)) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) f[k] = __dadd_rn(f[k], __ldcg(py + 4 + k));
+    }
+    if (FG && c <= (first == G ? G - 1 : first)) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) r[k] = __dadd_rn(r[k], __ldcg(py + 10 + k));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    f[k] = warp_sum(f[k]);
+    r[k] = warp_sum(r[k]);
+  }
+  if (lane == 0) {
+    P.shard_out[0] = last >= 0 ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      P.shard_out[1 + k] = f[k];
+      P.shard_out[4 + k] = r[k];
+    }
+    P.shard_out[7] = first == 0 ? 1.0 : 0.0;  // the shard's first tile starts a stratum
   }
 }
 
@@ -1344,20 +1394,25 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   }
   __syncthreads();
   if (tid == 0) {
-    int cs = 0;
+    int cs = 0, fs = 0;
     for (int c = cta - 1; c >= 0; --c)
       if (tl->cflag[c]) {
         cs = c;
+        fs = 1;
         break;
       }
-    int ce = G - 1;
+    int ce = G - 1, fe = 0;
     for (int c = cta + 1; c < G; ++c)
       if (tl->cflag[c]) {
         ce = c;
+        fe = 1;
         break;
       }
     tl->cstar = cs;
     tl->cend = ce;
+    // carry from other shards reaches this CTA when no stratum starts between
+    tl->ext_f = (P.ext && !fs) ? 1 : 0;
+    tl->ext_r = (P.ext && !fe) ? 1 : 0;
   }
 
   if (warp == W) {
@@ -1373,7 +1428,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   long long accepted = ctl->accepted, refreshes = ctl->refreshes, skipped = ctl->skipped;
   int err = ctl->err_code;
   long long err_col = ctl->err_col;
-  const bool rec_ok = P.mode == kModeCcd && ctl->rec_valid && ctl->rec_col == P.slot_col[0];
+  const bool rec_ok = (P.mode == kModeCcd || P.reuse_records) && ctl->rec_valid &&
+                      ctl->rec_col == P.slot_col[0];
   SlotState& ss = tl->ss;
   consumer_sync(NC);
   const int cstar = tl->cstar, cend = tl->cend;
@@ -1417,8 +1473,17 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   __threadfence();
   consumer_sync(NC);
   publish_exchange_gather(0.0, 0.0, 0.0);
+  if (P.shard_out && cta == 0 && warp == 0) shard_aggregate<FG>(P, rbuf(xi - 1), tl, lane);
+  if (P.prologue_only) {
+    if (tid == 0 && cta == 0) {
+      ctl->bar_base = bar_target;
+      ctl->rec_valid = err ? 0 : 1;  // the records serve the launch that follows
+      ctl->rec_col = P.slot_col[0];
+    }
+    return;
+  }
   if (tid == 0) {
-    set_carry_in<FG>(tl, 0.0);
+    set_carry_in<FG>(P, tl, 0.0);
     ss.pcol = -1;
     ss.delta = 0.0;
     ss.phi = 1.0;
@@ -1596,7 +1661,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       tl->bcast[3] = delta;
       tl->need_exact = need_exact;
       // provisional carries for slot k+1 (linear path)
-      set_carry_in<FG>(tl, (delta != 0.0) ? __dsub_rn(exp(delta), 1.0) : 0.0);
+      set_carry_in<FG>(P, tl, (delta != 0.0) ? __dsub_rn(exp(delta), 1.0) : 0.0);
     }
     consumer_sync(NC);
     double delta = tl->bcast[3];
@@ -1656,7 +1721,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
       publish_exchange_gather(0.0, 0.0, 0.0);
       if (tid == 0) {
-        set_carry_in<FG>(tl, 0.0);
+        set_carry_in<FG>(P, tl, 0.0);
         const double* pa = rbuf(xi - 1);
         double mm = 0.0;
         for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayStride + 16));
@@ -1668,7 +1733,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       __threadfence();
       consumer_sync(NC);
       publish_exchange_gather(0.0, 0.0, 0.0);
-      if (tid == 0) set_carry_in<FG>(tl, 0.0);
+      if (tid == 0) set_carry_in<FG>(P, tl, 0.0);
     }
     if (tid == 0) {
       ss.pcol = (delta != 0.0 && !tl->refresh) ? col : -1;

@@ -103,6 +103,13 @@ struct CycleParams {
   unsigned int trace_cap;
   int dbg;                     // debug/ablation bits (GSS_DEBUG): 1 skip tile work, 2 skip records,
                                // 4 skip scans/transform
+  // ---- patient sharding (C5): this engine holds one contiguous row shard ----
+  const double* ext;           // [8] carry from the other shards: fwd (a,b,c) into the first
+                               // tile, [4..6] rev (ua,ub,uc) after the last; NULL = none
+  double* shard_out;           // [8] this shard's aggregate after the prologue exchange:
+                               // [0] stratum-start flag, [1..3] fwd tail, [4..6] rev head
+  int prologue_only;           // stop after the prologue (records + shard aggregate)
+  int reuse_records;           // API mode: records from a prologue-only launch are valid
 };
 
 // launchers (gss_cycle.cu)
