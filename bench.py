@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--e2e-max-cycles", type=int, default=60)
     ap.add_argument("--cpu-sample-p", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c3-p", type=int, default=5000,
+                    help="columns of the secondary C3 (Fine-Gray) measurement; 0 = skip")
+    ap.add_argument("--c3-cycles", type=int, default=2)
     return ap.parse_args()
 
 
@@ -317,6 +320,7 @@ def run_gss(args, dist):
         ttf.append(wall)
         e2e_cycles.append(r2["cycles"])
         del e2, d2
+    c3 = run_c3(args, dist) if args.c3_p > 0 else None
     out = {
         "metric": "cox_ccd_coordinate_updates_per_s",
         "value": round(value, 2),
@@ -351,7 +355,40 @@ def run_gss(args, dist):
         "clocks": clocks,
         "fit_objective_after_timed_cycles": res["objective"],
     }
+    if c3 is not None:
+        out["secondary"] = {"c3_finegray": c3}
     return out
+
+
+def run_c3(args, dist):
+    """Config C3 (Fine-Gray, forward-backward scan with censoring weights) at
+    N=10M: device-timed coordinate updates/s over `c3_cycles` cycles after one
+    warm-up cycle; algorithmic bytes 20*N (+4*nnz_j) per coordinate (e, code, G)."""
+    from paper_2204_08183_b200 import capi
+    dev = dist.local
+    sim = capi.SimData(args.n, args.c3_p, args.density, 0.8, args.seed + 1 + dist.rank,
+                       args.censoring_quantile, args.quantum, device=dev, p_mix=0.5)
+    ds = capi.Dataset(sim.times, sim.status, sim.col_ptr, sim.row_idx, device=dev)
+    eng = capi.Engine(ds, "finegray")
+    W, K = 1, args.c3_cycles
+    eng.fit(penalty="l1", strength=args.strength, tol=1e-300, max_cycles=W + K)
+    ms, acc = eng.cycle_stats()
+    timed = float(ms[W:W + K].sum())
+    t_max = dist.max(timed)
+    value = dist.sum(float(K * args.c3_p)) / (t_max * 1e-3)
+    nnz = np.diff(sim.col_ptr).astype(np.float64)
+    per_coord = 20.0 * args.n + 4.0 * float(nnz.mean())
+    achieved = (per_coord * args.c3_p + 20.0 * args.n) * K / (timed * 1e-3) / 1e9
+    peak = json.load(open(PEAKS))["hbm_gbs"] if os.path.exists(PEAKS) else 6650.0
+    n_comp = int((sim.status == 2).sum())
+    return {"workload": f"C3: Fine-Gray, N={args.n}, p={args.c3_p}, 1% binary, p_mix=0.5, "
+                        f"ties q=1e-3, cq={args.censoring_quantile}, L1 gamma=sqrt(2)",
+            "value": round(value, 2), "unit": "coord_updates/s",
+            "ms_per_cycle": round(t_max / K, 3), "cycles_timed": K,
+            "competing_rows": n_comp,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_coordinate": round(per_coord, 1)}}
 
 
 def main():

@@ -19,6 +19,8 @@ typedef struct gss_sim_config {
   uint64_t seed;
   double censoring_quantile; /* administrative cutoff quantile, <= 0: none       */
   double time_quantum;       /* t <- ceil(t*q)/q (Breslow ties), <= 0: none      */
+  double p_mix;              /* > 0: Fine-Gray competing-risk design with primary
+                                mixture mass p_mix (simgen.hpp:33-37); 0: Cox   */
 } gss_sim_config;
 
 typedef struct gss_sim_out {
@@ -31,6 +33,8 @@ typedef struct gss_sim_out {
 } gss_sim_out;
 
 int gss_simulate_cox(const gss_sim_config* cfg, int device, gss_sim_out* out);
+/* same, Fine-Gray design when cfg->p_mix > 0 (status 2 = competing event) */
+int gss_simulate(const gss_sim_config* cfg, int device, gss_sim_out* out);
 void gss_sim_free(gss_sim_out* out);
 const char* gss_sim_last_error(void);
 

@@ -134,7 +134,8 @@ class Dataset:
 class SimConfig(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("p", ctypes.c_int64), ("density", ctypes.c_double),
                 ("beta_sparsity", ctypes.c_double), ("seed", ctypes.c_uint64),
-                ("censoring_quantile", ctypes.c_double), ("time_quantum", ctypes.c_double)]
+                ("censoring_quantile", ctypes.c_double), ("time_quantum", ctypes.c_double),
+                ("p_mix", ctypes.c_double)]
 
 
 class SimOut(ctypes.Structure):
@@ -151,12 +152,13 @@ class SimData:
     Arrays are zero-copy numpy views valid while this object lives."""
 
     def __init__(self, n, p, density=0.01, beta_sparsity=0.8, seed=0, censoring_quantile=0.0,
-                 time_quantum=0.0, device=0):
+                 time_quantum=0.0, device=0, p_mix=0.0):
         L = lib()
         L.gss_sim_last_error.restype = ctypes.c_char_p
         self._out = SimOut()
-        cfg = SimConfig(n, p, density, beta_sparsity, seed, censoring_quantile, time_quantum)
-        rc = L.gss_simulate_cox(ctypes.byref(cfg), device, ctypes.byref(self._out))
+        cfg = SimConfig(n, p, density, beta_sparsity, seed, censoring_quantile, time_quantum,
+                        p_mix)
+        rc = L.gss_simulate(ctypes.byref(cfg), device, ctypes.byref(self._out))
         if rc:
             raise GssError(rc, L.gss_sim_last_error().decode())
         o = self._out

@@ -85,12 +85,38 @@ __global__ void rows_kernel(int64_t n, int64_t p, double density, uint64_t seed,
   }
 }
 
+// Cox: Exponential(rate exp(x'beta)).  Fine-Gray (p_mix > 0): the primary
+// event with probability 1 - (1 - p_mix)^exp(x'beta), its time by inverting the
+// subdistribution 1 - [1 - p_mix (1 - e^-t)]^exp(x'beta); otherwise a competing
+// event at Exponential(rate exp(-x'beta)) (simgen.hpp:33-37 design).
 __global__ void times_kernel(int64_t n, uint64_t seed, const double* __restrict__ eta,
-                             double* __restrict__ t, int64_t* __restrict__ ids) {
+                             double p_mix, double* __restrict__ t, int32_t* __restrict__ cause,
+                             int64_t* __restrict__ ids) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     Rng r(mix64(seed ^ 0x71d67fffeda60000ULL) ^ mix64(uint64_t(i) + 7));
-    t[i] = -log(r.uniform()) / exp(eta[i]);
+    const double rate = exp(eta[i]);
+    int32_t c = 1;
+    double ti;
+    if (p_mix <= 0.0) {
+      ti = -log(r.uniform()) / rate;
+    } else {
+      const double p1 = -expm1(rate * log1p(-p_mix));
+      if (r.uniform() < p1) {
+        ti = INFINITY;
+        for (int k = 0; k < 64 && !isfinite(ti); ++k) {
+          const double v = r.uniform() * p1;
+          const double w = -expm1(log1p(-v) / rate) / p_mix;
+          ti = -log1p(-w);
+        }
+        if (!isfinite(ti)) ti = 1e300;
+      } else {
+        ti = -log(r.uniform()) * rate;
+        c = 2;
+      }
+    }
+    t[i] = ti;
+    cause[i] = c;
     ids[i] = i;
   }
 }
@@ -100,7 +126,7 @@ __global__ void censor_kernel(int64_t n, double cutoff, double quantum, double* 
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     double ti = t[i];
-    int32_t s = 1;
+    int32_t s = status[i];  // cause from times_kernel
     if (cutoff > 0.0 && ti > cutoff) {
       ti = cutoff;
       s = 0;
@@ -177,6 +203,12 @@ void gss_sim_free(gss_sim_out* o) {
 }
 
 int gss_simulate_cox(const gss_sim_config* c, int device, gss_sim_out* o) {
+  gss_sim_config cc = *c;
+  cc.p_mix = 0.0;
+  return gss_simulate(&cc, device, o);
+}
+
+int gss_simulate(const gss_sim_config* c, int device, gss_sim_out* o) {
   std::memset(o, 0, sizeof(*o));
   if (c->n <= 0 || c->p < 0 || c->n >= (int64_t(1) << 31) || c->p >= (int64_t(1) << 31)) {
     g_sim_error = "bad dimensions";
@@ -224,7 +256,7 @@ int gss_simulate_cox(const gss_sim_config* c, int device, gss_sim_out* o) {
   SIM_CUDA(cudaMalloc(&status, sizeof(int32_t) * n));
   SIM_CUDA(cudaMalloc(&status_sorted, sizeof(int32_t) * n));
   SIM_CUDA(cudaMalloc(&inv, sizeof(int32_t) * n));
-  times_kernel<<<grid(n), 256, 0, s>>>(n, c->seed, eta, t, ids);
+  times_kernel<<<grid(n), 256, 0, s>>>(n, c->seed, eta, c->p_mix, t, status, ids);
   double cutoff = -1.0;
   if (c->censoring_quantile > 0.0 && c->censoring_quantile < 1.0) {
     // type-7 quantile of the event times (util.hpp:33-42)
