@@ -18,7 +18,7 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIBGSS = os.path.join(PKG, "libgss.so")
+LIBGSS = os.environ.get("GSS_LIB") or os.path.join(PKG, "libgss.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "gss_device.cuh"
 #include "gss_kernels.cuh"
@@ -120,6 +121,7 @@ struct Tail {
   int need_exact, refresh, valued;
   int cstar, cend;
   int ext_f, ext_r;
+  volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
 };
 
 template <bool FG>
@@ -265,14 +267,55 @@ __device__ __forceinline__ int32_t list_at(const int32_t* ls, const ListRef& L, 
 }
 
 // ---------------------------------------------------------------------------
+// watchdog: every spin-wait gives up after kWatchdogNs and traps with a
+// message, so a protocol bug surfaces as a launch error, never a hung device
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kWatchdogNs = 10ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  return ns;
+}
+__device__ unsigned* g_marks;  // unused placeholder
+__device__ __noinline__ void watchdog_trap(const char* what, unsigned a, unsigned b,
+                                           const volatile unsigned* marks = nullptr) {
+  if (marks)
+    printf("gss watchdog: %s stuck (cta %d thread %d: %u %u) marks %x %x %x %x | %x %x %x %x | "
+           "%x %x %x %x | %x %x %x %x | producer %x %x %x %x %x %x %x\n",
+           what, blockIdx.x, threadIdx.x, a, b, marks[0], marks[1], marks[2], marks[3], marks[4],
+           marks[5], marks[6], marks[7], marks[8], marks[9], marks[10], marks[11], marks[12],
+           marks[13], marks[14], marks[15], marks[16], marks[17], marks[18], marks[19], marks[20],
+           marks[21], marks[22]);
+  else
+    printf("gss watchdog: %s stuck (cta %d thread %d: %u %u)\n", what, blockIdx.x, threadIdx.x,
+           a, b);
+  __trap();
+}
+
+// ---------------------------------------------------------------------------
 // grid barrier over the co-resident CTAs (monotonic counter, no reset)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned target) {
   __threadfence();
   atomicAdd(bar, 1u);
+  const unsigned long long t0 = gtimer();
+  unsigned it = 0;
   while (static_cast<int>(ld_acquire_u32(bar) - target) < 0) {
+    if ((++it & 1023u) == 0 && gtimer() - t0 > 2 * kWatchdogNs)
+      watchdog_trap("grid barrier", ld_acquire_u32(bar), target);
   }
   __threadfence();
+}
+
+// bounded wait on an mbarrier phase (consumers: data landed)
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what,
+                                             unsigned info,
+                                             const volatile unsigned* marks = nullptr) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = gtimer();
+  while (!mbar_try_wait(bar, parity)) {
+    if (gtimer() - t0 > kWatchdogNs) watchdog_trap(what, info, parity, marks);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -303,11 +346,11 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
   // every stage is awaited exactly one phase back and the S loads issue in parallel
   for (long long q0 = 0; q0 < total; q0 += G::kS) {
     const long long qq = q0 + lane;
+    long long lo[3] = {0, 0, 0};
+    int cnt[3] = {0, 0, 0};
     if (lane < G::kS && qq < total) {
       const int slot = static_cast<int>(qq / tc);
       const int tile = t0 + static_cast<int>(qq % tc);
-      long long lo[3] = {0, 0, 0};
-      int cnt[3] = {0, 0, 0};
       long long cols[3];
       cols[0] = (P.mode == kModeCcd && slot > 0) ? P.slot_col[slot - 1] : -1;
       cols[1] = P.slot_col[slot];
@@ -323,22 +366,40 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
           cnt[l] = static_cast<int>(b - a);
         }
       }
+    }
+    // lane 0 performs the waits in stage order (no lane-divergent mbarrier
+    // spinning inside the warp); lane i issues position q0+i as soon as its
+    // stage is free
+    for (int i = 0; i < G::kS && q0 + i < total; ++i) {
+      if (lane == 0) {
+        const long long qw = q0 + i;
+        const int sw = static_cast<int>(qw % G::kS);
+        const uint32_t phw = static_cast<uint32_t>((qw / G::kS) & 1);
+        tl->mark[16 + i] = 0xA0u | (static_cast<unsigned>(qw) << 8);
+        mbar_wait_wd(&tl->empty[sw], phw ^ 1, "producer empty-stage wait",
+                     static_cast<unsigned>(qw), tl->mark);
+        // the same tile of the previous slot must have committed its pending
+        // update before this slot's copy is read
+        if (qw >= tc) {
+          const long long prevq = qw - tc;
+          const int w = static_cast<int>((prevq % tc) % G::kNG);
+          const volatile unsigned* pr = &tl->progress[w];
+          const unsigned long long tw = gtimer();
+          while (static_cast<long long>(*pr) < prevq + 1) {
+            __nanosleep(32);
+            if (gtimer() - tw > kWatchdogNs)
+              watchdog_trap("producer progress wait", static_cast<unsigned>(qw), *pr, tl->mark);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+      }
+      __syncwarp();
+      if (lane != i) continue;
+      const int slot = static_cast<int>(qq / tc);
+      const int tile = t0 + static_cast<int>(qq % tc);
       const int s = static_cast<int>(qq % G::kS);
-      const uint32_t ph = static_cast<uint32_t>((qq / G::kS) & 1);
-      trace_c0(P, 24, static_cast<int>(qq));
-      while (!mbar_try_wait(&tl->empty[s], ph ^ 1)) {
-      }
-      trace_c0(P, 25, static_cast<int>(qq));
-      // the same tile of the previous slot must have committed its pending
-      // update before this slot's copy is read
-      if (qq >= tc) {
-        const long long prevq = qq - tc;
-        const int w = static_cast<int>((prevq % tc) % G::kNG);
-        const volatile unsigned* pr = &tl->progress[w];
-        while (static_cast<long long>(*pr) < prevq + 1) __nanosleep(32);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
       trace_c0(P, 23, static_cast<int>(qq));
+      tl->mark[16 + lane] = 0xC0u | (static_cast<unsigned>(qq) << 8);
       unsigned char* sb = smem + size_t(s) * G::kStage;
       StageInfo& inf = tl->info[s];
       inf.tile = tile;
@@ -376,6 +437,7 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         if (lbytes[l])
           bulk_load_1d(lbase + l * kNnzCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
       trace_c0(P, 26, static_cast<int>(qq));
+      tl->mark[16 + lane] = 0xD0u | (static_cast<unsigned>(qq) << 8) | (bytes >> 24);
     }
     __syncwarp();
   }
@@ -389,6 +451,11 @@ template <int L>
 struct Lanes {
   double v[L];
 };
+
+template <bool FG>
+__device__ __forceinline__ void mark(Tail<FG>* tl, unsigned code) {
+  if ((threadIdx.x & 31) == 0) tl->mark[threadIdx.x >> 5] = code;
+}
 
 template <bool FG>
 __device__ __forceinline__ void group_sync(int g) {
@@ -481,6 +548,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       atomicOr(&xn[lr >> 3], 1u << (lr & 7));
     }
   }
+  mark<FG>(tl, 0x11u | (static_cast<unsigned>(t & 0xffff) << 8));
   group_sync<FG>(g);
   trace_w0(P, 10, t);
 
@@ -615,6 +683,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     for (int i = 0; i < L; ++i) tl->gx[g][gw][i] = wt.v[i];
   }
   const unsigned wany = __reduce_or_sync(0xffffffffu, work);
+  mark<FG>(tl, 0x12u | (static_cast<unsigned>(t & 0xffff) << 8));
   group_sync<FG>(g);
   // offset of this warp's passes inside the tile (fixed order) and the tile total
   Lanes<L> off, ttot;
@@ -781,6 +850,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       for (int i = 0; i < NR; ++i) tl->gr[g][gw][i] = rv[i];
     }
   }
+  mark<FG>(tl, 0x13u | (static_cast<unsigned>(t & 0xffff) << 8));
   if constexpr (!FUSED) group_sync<FG>(g);
   if (!FUSED && gw == 0 && lane == 0 && !(P.dbg & 2)) {
     constexpr int NR = FG ? 10 : 5;
@@ -1277,13 +1347,11 @@ __device__ __noinline__ void gather_payloads(const CycleParams& P, const double*
     for (int i = 0; i < NV; ++i) tl->wred[warp][i] = v[i];
   }
   consumer_sync(NC);
-  if (tid == 0) {
-#pragma unroll 1
-    for (int i = 0; i < NV; ++i) {
-      double r = 0.0;
-      for (int w = 0; w < W; ++w) r = __dadd_rn(r, tl->wred[w][i]);
-      tl->gs[i] = r;
-    }
+  if (tid < NV) {  // one thread per value, warps in fixed order
+    double r = 0.0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) r = __dadd_rn(r, tl->wred[w][tid]);
+    tl->gs[tid] = r;
   }
   consumer_sync(NC);
 }
@@ -1442,6 +1510,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   // CTA barrier first (orders every thread's writes before thread 0), then one
   // gpu-scope fence + release by thread 0 (the cooperative-groups grid.sync pattern)
   auto exchange = [&]() {
+    mark<FG>(tl, 0x20u | (static_cast<unsigned>(xi) << 8));
     consumer_sync(NC);
     if (tid == 0) {
       trace_cta(P, 31, xtr, 29);
@@ -1468,6 +1537,19 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     gather_payloads<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, tid);
   };
 
+  // slot fields of slot kk (thread 0; read by the consumers after a barrier)
+  auto set_slot_fields = [&](int kk) {
+    if (kk >= P.nslots) return;
+    const long long c = P.slot_col[kk];
+    const long long nc =
+        (kk + 1 < P.nslots) ? P.slot_col[kk + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
+    ss.col = c;
+    ss.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
+    ss.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
+    ss.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
+    ss.fused = (!FG && P.mode == kModeCcd && c >= 0 && nc >= 0 && ss.cind && ss.nind &&
+                !(P.dbg & 8)) ? 1 : 0;
+  };
   // ---- prologue: records for slot 0 and the slot-0 carries ----
   if (!rec_ok) records_from_global<FG>(P, t0, tc, P.slot_col[0], warp, lane);
   __threadfence();
@@ -1490,8 +1572,36 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     ss.pind = 1;
     ss.refresh = 0;
     ss.dry = err ? 1 : 0;
+    set_slot_fields(0);
   }
+  consumer_sync(NC);
 
+  // accept the update: beta_[column] += delta, refresh cadence (src/engine.cpp:216-217)
+  auto accept = [&](double d, double bj, int ind, long long c) {
+    int do_refresh = 0;
+    if (d != 0.0) {
+      if (cta == 0) P.beta[c] = __dadd_rn(bj, d);
+      slack = __dadd_rn(slack, tl->bcast[5]);
+      ++accepted;
+      if (accepted % P.recompute_interval == 0) {
+        do_refresh = 1;  // refresh subsumes the incremental update
+        ++refreshes;
+      }
+    }
+    tl->refresh = do_refresh;
+    tl->valued = (d != 0.0 && !do_refresh && !ind) ? 1 : 0;
+  };
+  // the next slot's pending update and fields (thread 0)
+  auto finish_slot = [&](double d, int ind, long long c, int kk) {
+    ss.pcol = (d != 0.0 && !tl->refresh) ? c : -1;
+    ss.delta = d;
+    ss.phi = (d != 0.0) ? exp(d) : 1.0;
+    ss.pind = ind;
+    ss.refresh = tl->refresh;
+    ss.dry = err ? 1 : 0;
+    set_slot_fields(kk + 1);
+    trace_c0(P, 5, kk);
+  };
   long long qbase = 0;  // stream position of the slot's first tile
   int gpar = 0;         // this warp's group: mask buffer of its next tile
   for (int k = 0; k < P.nslots; ++k) {
@@ -1508,20 +1618,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       in_cmax = __ldcg(P.colmax + col);
       in_pen = P.penalized[col];
       in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
-      ss.col = col;
-      ss.kind = kSlotGrad;
-      ss.cind = in_ind;
-    } else if (tid == 0) {
-      ss.col = col;
-      ss.kind = kSlotLoglik;
-      ss.cind = 1;
     }
-    if (tid == 0) {
-      ss.nind = ncol >= 0 ? ((!P.has_vals || P.col_ind[ncol]) ? 1 : 0) : 1;
-      ss.fused = (!FG && P.mode == kModeCcd && col >= 0 && ncol >= 0 && ss.cind && ss.nind &&
-                  !(P.dbg & 8)) ? 1 : 0;
-    }
-    consumer_sync(NC);
     // ---- consume this CTA's tiles of slot k (warp per tile, fixed order) ----
     double acc0 = 0.0, acc1 = 0.0;
     int bad = 0;
@@ -1538,10 +1635,12 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         const long long q = qbase + i;
         const int s = static_cast<int>(q % S);
         const uint32_t ph = static_cast<uint32_t>((q / S) & 1);
-        mbar_wait(&tl->full[s], ph);
+        mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", static_cast<unsigned>(q),
+                     lane == 0 ? tl->mark : nullptr);
         if (gt0(warp, lane, GWr)) trace_c0(P, 21, static_cast<int>(q));
         if (pend_q >= 0) {
           fence_proxy_async_global();
+          mark<FG>(tl, 0x14u | (static_cast<unsigned>(q & 0xffff) << 8));
           group_sync<FG>(g);
           if (gw == 0 && lane == 0)
             *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) =
@@ -1553,6 +1652,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
           released = consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1,
                                       bad, &tl->empty[s]);
         gpar ^= 1;
+        mark<FG>(tl, 0x15u | (static_cast<unsigned>(q & 0xffff) << 8));
         group_sync<FG>(g);
         if (gw == 0 && lane == 0) {
           trace_c0(P, 22, static_cast<int>(q));
@@ -1562,6 +1662,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
       if (pend_q >= 0) {
         fence_proxy_async_global();
+        mark<FG>(tl, 0x16u);
         group_sync<FG>(g);
         if (gw == 0 && lane == 0)
           *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = static_cast<unsigned>(pend_q + 1);
@@ -1660,8 +1761,12 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
       tl->bcast[3] = delta;
       tl->need_exact = need_exact;
-      // provisional carries for slot k+1 (linear path)
+      // carries for slot k+1 (linear path; refresh / valued paths redo them)
       set_carry_in<FG>(P, tl, (delta != 0.0) ? __dsub_rn(exp(delta), 1.0) : 0.0);
+      if (!need_exact) {
+        accept(delta, in_beta, in_ind, col);
+        if (!tl->refresh && !tl->valued) finish_slot(delta, in_ind, col, k);
+      }
     }
     consumer_sync(NC);
     double delta = tl->bcast[3];
@@ -1685,26 +1790,12 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
           if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
           tl->bcast[3] = 0.0;
         }
+        accept(tl->bcast[3], in_beta, in_ind, col);
+        if (!tl->refresh && !tl->valued) finish_slot(tl->bcast[3], in_ind, col, k);
       }
       consumer_sync(NC);
       delta = tl->bcast[3];
     }
-    // ---- accept: beta_[column] += delta, refresh cadence (src/engine.cpp:216-217) ----
-    if (tid == 0) {
-      int do_refresh = 0;
-      if (delta != 0.0) {
-        if (cta == 0) P.beta[col] = __dadd_rn(in_beta, delta);
-        slack = __dadd_rn(slack, tl->bcast[5]);
-        ++accepted;
-        if (accepted % P.recompute_interval == 0) {
-          do_refresh = 1;  // refresh subsumes the incremental update
-          ++refreshes;
-        }
-      }
-      tl->refresh = do_refresh;
-      tl->valued = (delta != 0.0 && !do_refresh && !in_ind) ? 1 : 0;
-    }
-    consumer_sync(NC);
     if (tl->refresh) {
       const double mx = refresh_tiles<FG>(P, t0, tc, col, delta, ncol, warp, lane);
       fence_proxy_async_global();
@@ -1735,16 +1826,10 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       publish_exchange_gather(0.0, 0.0, 0.0);
       if (tid == 0) set_carry_in<FG>(P, tl, 0.0);
     }
-    if (tid == 0) {
-      ss.pcol = (delta != 0.0 && !tl->refresh) ? col : -1;
-      ss.delta = delta;
-      ss.phi = (delta != 0.0) ? exp(delta) : 1.0;
-      ss.pind = in_ind;
-      ss.refresh = tl->refresh;
-      ss.dry = err ? 1 : 0;
-      trace_c0(P, 5, k);
+    if (tl->refresh || tl->valued) {
+      if (tid == 0) finish_slot(delta, in_ind, col, k);
+      consumer_sync(NC);
     }
-    consumer_sync(NC);
   }
 
   // ---- epilogue: CTA 0 persists the replicated state ----
