@@ -97,6 +97,25 @@ struct SlotState {
   double cin_r[6];   // corrected rev carry into the CTA range (ua,ub,uc)
 };
 
+struct SlotFields {
+  long long col;
+  int kind, cind, nind, fused, valid;
+};
+
+// replicated CCD state, owned by thread 0 (kept in shared memory: registers
+// holding it across the consume phase would spill to local memory, which
+// misses L1 under this shared-memory carve-out)
+struct CcdState {
+  double absmax, slack;
+  long long accepted, refreshes, skipped, err_col;
+  int err;
+  unsigned bar_target;
+  // step inputs of the current slot, prefetched at slot start
+  double in_fixed, in_beta, in_hw, in_cmax;
+  int in_pen, in_ind;
+  SlotFields nf;
+};
+
 template <bool FG>
 struct Tail {
   static constexpr int W = Geo<FG>::kW, S = Geo<FG>::kS;
@@ -122,6 +141,7 @@ struct Tail {
   int cstar, cend;
   int ext_f, ext_r;
   volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
+  CcdState cs;
 };
 
 template <bool FG>
@@ -314,6 +334,7 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
   if (mbar_try_wait(bar, parity)) return;
   const unsigned long long t0 = gtimer();
   while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(64);  // back off: spinning waiters would steal the producer's issue slots
     if (gtimer() - t0 > kWatchdogNs) watchdog_trap(what, info, parity, marks);
   }
 }
@@ -339,18 +360,22 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
                                       int t0, int tc, const CUtensorMap* tm_e,
                                       const CUtensorMap* tm_code, const CUtensorMap* tm_g) {
   using G = Geo<FG>;
+  constexpr int S = G::kS;
   const int lane = threadIdx.x & 31;
-  const long long total = static_cast<long long>(P.nslots) * tc;
+  // positions are 32-bit (slots x tiles-per-CTA < 2^31): no 64-bit divisions
+  const unsigned total = static_cast<unsigned>(P.nslots) * static_cast<unsigned>(tc);
   const size_t nt1 = static_cast<size_t>(P.ntiles) + 1;
-  // waves of S positions: lane l < S owns position q0 + l (stage (q0 + l) % S), so
-  // every stage is awaited exactly one phase back and the S loads issue in parallel
-  for (long long q0 = 0; q0 < total; q0 += G::kS) {
-    const long long qq = q0 + lane;
+  const unsigned utc = static_cast<unsigned>(tc);
+  // waves of S positions; lane l < S owns position q0 + l (stage l of the wave)
+  for (unsigned q0 = 0; q0 < total; q0 += S) {
+    const unsigned qq = q0 + lane;
     long long lo[3] = {0, 0, 0};
     int cnt[3] = {0, 0, 0};
-    if (lane < G::kS && qq < total) {
-      const int slot = static_cast<int>(qq / tc);
-      const int tile = t0 + static_cast<int>(qq % tc);
+    int slot = 0, tloc = 0;
+    if (lane < S && qq < total) {
+      slot = static_cast<int>(qq / utc);
+      tloc = static_cast<int>(qq - static_cast<unsigned>(slot) * utc);
+      const int tile = t0 + tloc;
       long long cols[3];
       cols[0] = (P.mode == kModeCcd && slot > 0) ? P.slot_col[slot - 1] : -1;
       cols[1] = P.slot_col[slot];
@@ -367,39 +392,40 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         }
       }
     }
+    const uint32_t phase = (q0 / S) & 1u;  // every position of the wave shares it
     // lane 0 performs the waits in stage order (no lane-divergent mbarrier
     // spinning inside the warp); lane i issues position q0+i as soon as its
     // stage is free
-    for (int i = 0; i < G::kS && q0 + i < total; ++i) {
+    for (int i = 0; i < S; ++i) {
+      if (q0 + i >= total) break;
+      const int tl_i = __shfl_sync(0xffffffffu, tloc, i);
       if (lane == 0) {
-        const long long qw = q0 + i;
-        const int sw = static_cast<int>(qw % G::kS);
-        const uint32_t phw = static_cast<uint32_t>((qw / G::kS) & 1);
-        tl->mark[16 + i] = 0xA0u | (static_cast<unsigned>(qw) << 8);
-        mbar_wait_wd(&tl->empty[sw], phw ^ 1, "producer empty-stage wait",
-                     static_cast<unsigned>(qw), tl->mark);
+        const unsigned qw = q0 + i;
+        tl->mark[16 + i] = 0xA0u | (qw << 8);
+        trace_c0(P, 24, static_cast<int>(qw));
+        mbar_wait_wd(&tl->empty[i], phase ^ 1u, "producer empty-stage wait", qw, tl->mark);
+        trace_c0(P, 25, static_cast<int>(qw));
         // the same tile of the previous slot must have committed its pending
-        // update before this slot's copy is read
-        if (qw >= tc) {
-          const long long prevq = qw - tc;
-          const int w = static_cast<int>((prevq % tc) % G::kNG);
-          const volatile unsigned* pr = &tl->progress[w];
-          const unsigned long long tw = gtimer();
-          while (static_cast<long long>(*pr) < prevq + 1) {
-            __nanosleep(32);
-            if (gtimer() - tw > kWatchdogNs)
-              watchdog_trap("producer progress wait", static_cast<unsigned>(qw), *pr, tl->mark);
+        // update (the committing group fenced generic -> async proxy before
+        // publishing its progress)
+        if (qw >= utc) {
+          const unsigned prevq = qw - utc;
+          const volatile unsigned* pr = &tl->progress[tl_i % G::kNG];
+          if (*pr < prevq + 1) {
+            const unsigned long long tw = gtimer();
+            while (*pr < prevq + 1) {
+              __nanosleep(32);
+              if (gtimer() - tw > kWatchdogNs)
+                watchdog_trap("producer progress wait", qw, *pr, tl->mark);
+            }
           }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
         }
       }
       __syncwarp();
       if (lane != i) continue;
-      const int slot = static_cast<int>(qq / tc);
-      const int tile = t0 + static_cast<int>(qq % tc);
-      const int s = static_cast<int>(qq % G::kS);
+      const int tile = t0 + tloc;
+      const int s = i;
       trace_c0(P, 23, static_cast<int>(qq));
-      tl->mark[16 + lane] = 0xC0u | (static_cast<unsigned>(qq) << 8);
       unsigned char* sb = smem + size_t(s) * G::kStage;
       StageInfo& inf = tl->info[s];
       inf.tile = tile;
@@ -437,7 +463,7 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         if (lbytes[l])
           bulk_load_1d(lbase + l * kNnzCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
       trace_c0(P, 26, static_cast<int>(qq));
-      tl->mark[16 + lane] = 0xD0u | (static_cast<unsigned>(qq) << 8) | (bytes >> 24);
+      tl->mark[16 + lane] = 0xD0u | (qq << 8);
     }
     __syncwarp();
   }
@@ -1490,12 +1516,25 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
 
   // ------------------------- consumer / control warps ----------------------
   // replicated CCD state (identical in every CTA: same inputs, same order)
-  unsigned bar_target = static_cast<unsigned>(ctl->bar_base);
-  double absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
-  double slack = ctl->bound_slack;
-  long long accepted = ctl->accepted, refreshes = ctl->refreshes, skipped = ctl->skipped;
-  int err = ctl->err_code;
-  long long err_col = ctl->err_col;
+  CcdState& cst = tl->cs;
+  if (tid == 0) {
+    cst.bar_target = static_cast<unsigned>(ctl->bar_base);
+    cst.absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
+    cst.slack = ctl->bound_slack;
+    cst.accepted = ctl->accepted;
+    cst.refreshes = ctl->refreshes;
+    cst.skipped = ctl->skipped;
+    cst.err = ctl->err_code;
+    cst.err_col = ctl->err_col;
+  }
+  unsigned& bar_target = cst.bar_target;
+  double& absmax = cst.absmax;
+  double& slack = cst.slack;
+  long long& accepted = cst.accepted;
+  long long& refreshes = cst.refreshes;
+  long long& skipped = cst.skipped;
+  int& err = cst.err;
+  long long& err_col = cst.err_col;
   const bool rec_ok = (P.mode == kModeCcd || P.reuse_records) && ctl->rec_valid &&
                       ctl->rec_col == P.slot_col[0];
   SlotState& ss = tl->ss;
@@ -1534,21 +1573,34 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
     }
     exchange();
+    if (tid == 0) trace_c0(P, 8, 0);
     gather_payloads<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, tid);
+    if (tid == 0) trace_c0(P, 9, 0);
   };
 
   // slot fields of slot kk (thread 0; read by the consumers after a barrier)
-  auto set_slot_fields = [&](int kk) {
-    if (kk >= P.nslots) return;
+  auto slot_fields = [&](int kk) {
+    SlotFields f{};
+    f.valid = kk < P.nslots;
+    if (!f.valid) return f;
     const long long c = P.slot_col[kk];
     const long long nc =
         (kk + 1 < P.nslots) ? P.slot_col[kk + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
-    ss.col = c;
-    ss.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
-    ss.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
-    ss.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
-    ss.fused = (!FG && P.mode == kModeCcd && c >= 0 && nc >= 0 && ss.cind && ss.nind &&
-                !(P.dbg & 8)) ? 1 : 0;
+    f.col = c;
+    f.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
+    f.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
+    f.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
+    f.fused = (!FG && P.mode == kModeCcd && c >= 0 && nc >= 0 && f.cind && f.nind &&
+               !(P.dbg & 8)) ? 1 : 0;
+    return f;
+  };
+  auto set_slot_fields = [&](const SlotFields& f) {
+    if (!f.valid) return;
+    ss.col = f.col;
+    ss.kind = f.kind;
+    ss.cind = f.cind;
+    ss.nind = f.nind;
+    ss.fused = f.fused;
   };
   // ---- prologue: records for slot 0 and the slot-0 carries ----
   if (!rec_ok) records_from_global<FG>(P, t0, tc, P.slot_col[0], warp, lane);
@@ -1572,7 +1624,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     ss.pind = 1;
     ss.refresh = 0;
     ss.dry = err ? 1 : 0;
-    set_slot_fields(0);
+    set_slot_fields(slot_fields(0));
   }
   consumer_sync(NC);
 
@@ -1592,14 +1644,14 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     tl->valued = (d != 0.0 && !do_refresh && !ind) ? 1 : 0;
   };
   // the next slot's pending update and fields (thread 0)
-  auto finish_slot = [&](double d, int ind, long long c, int kk) {
+  auto finish_slot = [&](double d, double phi, int ind, long long c, const SlotFields& nf, int kk) {
     ss.pcol = (d != 0.0 && !tl->refresh) ? c : -1;
     ss.delta = d;
-    ss.phi = (d != 0.0) ? exp(d) : 1.0;
+    ss.phi = phi;
     ss.pind = ind;
     ss.refresh = tl->refresh;
     ss.dry = err ? 1 : 0;
-    set_slot_fields(kk + 1);
+    set_slot_fields(nf);
     trace_c0(P, 5, kk);
   };
   long long qbase = 0;  // stream position of the slot's first tile
@@ -1609,15 +1661,25 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     const long long ncol =
         (k + 1 < P.nslots) ? P.slot_col[k + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
     // step inputs, loaded now and used after the exchange (latency hidden)
-    double in_fixed = 0.0, in_beta = 0.0, in_hw = 0.0, in_cmax = 0.0;
-    int in_pen = 0, in_ind = 1;
-    if (tid == 0 && col >= 0) {
-      in_fixed = __ldcg(P.fixed + col);
-      in_beta = __ldcg(P.beta + col);
-      in_hw = __ldcg(P.halfwidth + col);
-      in_cmax = __ldcg(P.colmax + col);
-      in_pen = P.penalized[col];
-      in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
+    double& in_fixed = cst.in_fixed;
+    double& in_beta = cst.in_beta;
+    double& in_hw = cst.in_hw;
+    double& in_cmax = cst.in_cmax;
+    int& in_pen = cst.in_pen;
+    int& in_ind = cst.in_ind;
+    SlotFields& nf = cst.nf;
+    if (tid == 0) {
+      in_ind = 1;
+      if (col >= 0) {
+        in_fixed = __ldcg(P.fixed + col);
+        in_beta = __ldcg(P.beta + col);
+        in_hw = __ldcg(P.halfwidth + col);
+        in_cmax = __ldcg(P.colmax + col);
+        in_pen = P.penalized[col];
+        in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
+      }
+      // the next slot's fields, resolved now (off the post-exchange critical path)
+      nf = slot_fields(k + 1);
     }
     // ---- consume this CTA's tiles of slot k (warp per tile, fixed order) ----
     double acc0 = 0.0, acc1 = 0.0;
@@ -1632,9 +1694,9 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       // time the commit stores have drained; the slot's last tile is flushed below.
       long long pend_q = -1;
       for (int i = g; i < tc; i += NGr) {
-        const long long q = qbase + i;
+        const unsigned q = static_cast<unsigned>(qbase) + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
-        const uint32_t ph = static_cast<uint32_t>((q / S) & 1);
+        const uint32_t ph = (q / S) & 1u;
         mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", static_cast<unsigned>(q),
                      lane == 0 ? tl->mark : nullptr);
         if (gt0(warp, lane, GWr)) trace_c0(P, 21, static_cast<int>(q));
@@ -1761,11 +1823,13 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
       tl->bcast[3] = delta;
       tl->need_exact = need_exact;
+      const double phi = (delta != 0.0) ? exp(delta) : 1.0;
+      tl->bcast[6] = phi;
       // carries for slot k+1 (linear path; refresh / valued paths redo them)
-      set_carry_in<FG>(P, tl, (delta != 0.0) ? __dsub_rn(exp(delta), 1.0) : 0.0);
+      set_carry_in<FG>(P, tl, __dsub_rn(phi, 1.0));
       if (!need_exact) {
         accept(delta, in_beta, in_ind, col);
-        if (!tl->refresh && !tl->valued) finish_slot(delta, in_ind, col, k);
+        if (!tl->refresh && !tl->valued) finish_slot(delta, phi, in_ind, col, nf, k);
       }
     }
     consumer_sync(NC);
@@ -1790,8 +1854,9 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
           if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
           tl->bcast[3] = 0.0;
         }
+        if (tl->bcast[3] == 0.0) tl->bcast[6] = 1.0;
         accept(tl->bcast[3], in_beta, in_ind, col);
-        if (!tl->refresh && !tl->valued) finish_slot(tl->bcast[3], in_ind, col, k);
+        if (!tl->refresh && !tl->valued) finish_slot(tl->bcast[3], tl->bcast[6], in_ind, col, nf, k);
       }
       consumer_sync(NC);
       delta = tl->bcast[3];
@@ -1827,7 +1892,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       if (tid == 0) set_carry_in<FG>(P, tl, 0.0);
     }
     if (tl->refresh || tl->valued) {
-      if (tid == 0) finish_slot(delta, in_ind, col, k);
+      if (tid == 0) finish_slot(delta, tl->bcast[6], in_ind, col, nf, k);
       consumer_sync(NC);
     }
   }

@@ -121,20 +121,22 @@ if n > 2:
         np.median(arr.max(1) - arr.min(1)), np.median(pas_.min(1) - last_arrive),
         np.median(pas_.max(1) - last_arrive)))
 top, aft_empty, aft_issue = by_arg(24), by_arg(25), by_arg(26)
-qq = sorted(set(top) & set(aft_empty) & set(pas) & set(iss) & set(aft_issue))
+qq = sorted(set(top) & set(aft_empty) & set(iss) & set(aft_issue))
+pas = {q: aft_empty[q] for q in qq}
 def med(xs):
     return round(float(np.median(xs)), 3) if len(xs) else None
 print("producer per position (median us): wait-empty", med([aft_empty[q] - top[q] for q in qq]),
+      "| empty->issue-start", med([iss[q] - aft_empty[q] for q in qq]),
       "| progress", med([pas[q] - aft_empty[q] for q in qq]),
       "| setup", med([iss[q] - pas[q] for q in qq]),
       "| issue", med([aft_issue[q] - iss[q] for q in qq]),
       "| to next top", med([top[q + 1] - aft_issue[q] for q in qq if q + 1 in top]))
-# raw timeline of one middle slot on CTA 0
-tc_ = 33
+# raw timeline of one middle slot on CTA 0 (CTA 0 owns floor(ntiles/G) tiles)
+tc_ = (((a.n + 2047) // 2048)) // 148
 sl = 40
 c5d = by_arg(5)
 if sl - 1 in c5d:
-    base = c5d[sl - 1]
+    base = c5d[sl - 1]  # previous slot's control done
     print("slot %d timeline (us from previous slot done): q: issue / data / release" % sl)
     rows_ = []
     for i in range(tc_):
@@ -145,3 +147,11 @@ if sl - 1 in c5d:
         print("   " + "  ".join(rows_[j:j + 4]))
     print("   slot consumed at %.2f, exchange passed %.2f, done %.2f" % (
         by_arg(3).get(sl, np.nan) - base, by_arg(4).get(sl, np.nan) - base, c5d.get(sl, np.nan) - base))
+
+# post-exchange breakdown on CTA 0: 4 passed -> 8 after barrier release (tid 0) -> 9 gathered -> 5 slot done
+e8 = np.sort(t_us[kind == 8]); e9 = np.sort(t_us[kind == 9]); e5 = np.sort(t_us[kind == 5])
+if len(e8) > 10 and len(e9) == len(e8):
+    g = e9 - e8
+    # pair each gather end with the next slot-done event
+    d = [e5[np.searchsorted(e5, x)] - x for x in e9 if np.searchsorted(e5, x) < len(e5)]
+    print("post-exchange: gather %.2f us, step+carries+sync %.2f us (medians)" % (np.median(g), np.median(d)))
