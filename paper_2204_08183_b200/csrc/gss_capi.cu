@@ -148,6 +148,7 @@ struct gss_engine {
   double *trec = nullptr, *tcar = nullptr, *cpay = nullptr, *slot_out = nullptr;
   double *ext = nullptr, *shard = nullptr;  // patient-shard carry in / aggregate out
   int32_t* slot_col = nullptr;
+  int32_t* cta_tile0 = nullptr;
   unsigned int* bar = nullptr;
   Ctl* ctl = nullptr;
   int* dflag = nullptr;
@@ -166,7 +167,7 @@ struct gss_engine {
     for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
                     (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
                     (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
-                    (void*)dflag, (void*)ext, (void*)shard})
+                    (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0})
       if (q) cudaFree(q);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (ev0) cudaEventDestroy(ev0);
@@ -675,6 +676,42 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.pen_strength = 0.0;
   P.recompute_interval = recompute_interval;
   P.grid = E->grid;
+  {
+    // cost-balanced contiguous tile ranges: a tile costs its streaming (1)
+    // plus transform passes (8-row x 32-lane passes holding a tied-block end)
+    std::vector<double> w(static_cast<size_t>(nt), 1.0);
+    for (int t = 0; t < nt; ++t) {
+      int work = 0;
+      for (int pass = 0; pass < kTileRows / 256; ++pass) {
+        bool any = false;
+        for (int r = 0; r < 256 && !any; ++r)
+          any = (E->h_code[size_t(t) * kTileRows + pass * 256 + r] & kCodeCount) != 0;
+        work += any ? 1 : 0;
+      }
+      static const double kPassW = std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
+      w[t] = 1.0 + kPassW * work;
+    }
+    double tot = 0.0;
+    for (double x : w) tot += x;
+    std::vector<int32_t> t0(static_cast<size_t>(E->grid) + 1, 0);
+    double acc = 0.0;
+    int c = 1;
+    for (int t = 0; t < nt && c < E->grid; ++t) {
+      acc += w[t];
+      // cut after tile t once CTA c-1 holds its share (every CTA keeps >= 1 tile)
+      while (c < E->grid && acc >= tot * c / E->grid && t + 1 <= nt - (E->grid - c)) {
+        t0[c] = t + 1;
+        ++c;
+      }
+    }
+    for (; c < E->grid; ++c) t0[c] = std::max(t0[c - 1] + 1, nt - (E->grid - c));
+    t0[E->grid] = nt;
+    for (int k = 1; k <= E->grid; ++k)
+      if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
+    EK(dalloc(&E->cta_tile0, E->grid + 1));
+    EK(cudaMemcpy(E->cta_tile0, t0.data(), (E->grid + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+    P.cta_tile0 = E->cta_tile0;
+  }
   P.trec = E->trec;
   P.tcar = E->tcar;
   P.cpay = E->cpay;

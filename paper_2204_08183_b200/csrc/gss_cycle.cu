@@ -1460,8 +1460,11 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x;
   const int G = P.grid;
+  // static contiguous tile ranges, balanced by estimated tile cost (host,
+  // per engine); P.cta_tile0[c] = first tile of CTA c, [G] = ntiles
   auto range_lo = [&](int c) {
-    return static_cast<int>((static_cast<long long>(c) * P.ntiles) / G);
+    return P.cta_tile0 ? P.cta_tile0[c]
+                       : static_cast<int>((static_cast<long long>(c) * P.ntiles) / G);
   };
   const int t0 = range_lo(cta);
   const int tc = range_lo(cta + 1) - t0;

@@ -90,6 +90,7 @@ struct CycleParams {
   int nslots;
   int mode;                    // LaunchMode
   int grid;                    // CTAs (<= co-resident capacity)
+  const int32_t* cta_tile0;    // [grid+1] first tile of each CTA (cost-balanced), or NULL
   double* slot_out;            // optional [nslots][4] API results (gradient, hessian, fixed, ll)
   // ---- scratch ----
   double* trec;                // [ntiles][kRecStride]
