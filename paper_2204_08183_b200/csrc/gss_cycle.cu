@@ -1691,46 +1691,30 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     {
       constexpr int NGr = Gm::kNG, GWr = Gm::kGW;
       const int g = warp / GWr, gw = warp % GWr;
-      // Progress (the producer's licence to reload a tile for the next slot) is
-      // published one tile late: the proxy fence ordering this tile's commits
-      // before that TMA read runs when the group starts its next tile, by which
-      // time the commit stores have drained; the slot's last tile is flushed below.
-      long long pend_q = -1;
+      // Progress (the producer's licence to reload a tile for the next slot)
+      // is published with the stage release; the threads that committed the
+      // pending update fence generic -> async proxy first (their stores were
+      // issued in the patch phase and have drained by now, so this is cheap).
       for (int i = g; i < tc; i += NGr) {
         const unsigned q = static_cast<unsigned>(qbase) + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
         const uint32_t ph = (q / S) & 1u;
-        mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", static_cast<unsigned>(q),
-                     lane == 0 ? tl->mark : nullptr);
+        mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", q, lane == 0 ? tl->mark : nullptr);
         if (gt0(warp, lane, GWr)) trace_c0(P, 21, static_cast<int>(q));
-        if (pend_q >= 0) {
-          fence_proxy_async_global();
-          mark<FG>(tl, 0x14u | (static_cast<unsigned>(q & 0xffff) << 8));
-          group_sync<FG>(g);
-          if (gw == 0 && lane == 0)
-            *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) =
-                static_cast<unsigned>(pend_q + 1);
-        }
         unsigned char* sb = smem + size_t(s) * Gm::kStage;
-        bool released = false;
         if (!dry && !(P.dbg & 1))
-          released = consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1,
-                                      bad, &tl->empty[s]);
+          consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1, bad,
+                           &tl->empty[s]);
         gpar ^= 1;
-        mark<FG>(tl, 0x15u | (static_cast<unsigned>(q & 0xffff) << 8));
+        if (ss.pcol >= 0 && !ss.refresh && (gw * 32 + lane) < tl->info[s].l[0].cnt)
+          fence_proxy_async_global();
+        mark<FG>(tl, 0x15u | (q << 8));
         group_sync<FG>(g);
         if (gw == 0 && lane == 0) {
           trace_c0(P, 22, static_cast<int>(q));
-          if (!released) mbar_arrive(&tl->empty[s]);
+          *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = q + 1;
+          mbar_arrive(&tl->empty[s]);
         }
-        pend_q = q;
-      }
-      if (pend_q >= 0) {
-        fence_proxy_async_global();
-        mark<FG>(tl, 0x16u);
-        group_sync<FG>(g);
-        if (gw == 0 && lane == 0)
-          *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = static_cast<unsigned>(pend_q + 1);
       }
     }
     qbase += tc;
