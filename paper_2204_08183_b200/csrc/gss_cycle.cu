@@ -59,14 +59,15 @@ struct Geo {
   static_assert(kPasses % kGW == 0 && kW % kGW == 0, "group geometry");
   static constexpr int kNG = kW / kGW;    // tile groups (tiles in process at once)
   static constexpr int kS = FG ? 4 : 7;   // ring stages
+  static constexpr int kCap = kNnzCap;    // per-list smem capacity (ints)
   static constexpr uint32_t kEBytes = kTileRows * 8;
   static constexpr uint32_t kCBytes = kTileRows * 4;
   static constexpr uint32_t kGBytes = FG ? kTileRows * 8 : 0;
-  static constexpr uint32_t kLBytes = kNnzCap * 4;
+  static constexpr uint32_t kLBytes = kCap * 4;
   static constexpr uint32_t kOffC = kEBytes;
   static constexpr uint32_t kOffG = kEBytes + kCBytes;
   static constexpr uint32_t kOffL = kEBytes + kCBytes + kGBytes;
-  static constexpr uint32_t kStage = kOffL + 3 * kLBytes;
+  static constexpr uint32_t kStage = (kOffL + 3 * kLBytes + 1023) / 1024 * 1024;
   static constexpr int kThreads = 32 * (kW + 1);
   static_assert(kStage % 1024 == 0, "stage alignment");
 };
@@ -441,7 +442,7 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         if (cnt[l] > 0) {
           const long long base = lo[l] & ~3LL;
           const long long end = (lo[l] + cnt[l] + 3) & ~3LL;
-          if (end - base <= kNnzCap) {
+          if (end - base <= G::kCap) {
             inf.l[l].off = static_cast<int>(lo[l] - base);
             lbytes[l] = static_cast<uint32_t>((end - base) * 4);
             bytes += lbytes[l];
@@ -461,7 +462,7 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
 #pragma unroll
       for (int l = 0; l < 3; ++l)
         if (lbytes[l])
-          bulk_load_1d(lbase + l * kNnzCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
+          bulk_load_1d(lbase + l * G::kCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
       trace_c0(P, 26, static_cast<int>(qq));
       tl->mark[16 + lane] = 0xD0u | (qq << 8);
     }
@@ -510,8 +511,8 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   const unsigned char* sg = sb + G::kOffG;
   const int32_t* lbase = reinterpret_cast<const int32_t*>(sb + G::kOffL);
   const int32_t* lp = lbase;
-  const int32_t* lcur = lbase + kNnzCap;
-  const int32_t* lnext = lbase + 2 * kNnzCap;
+  const int32_t* lcur = lbase + G::kCap;
+  const int32_t* lnext = lbase + 2 * G::kCap;
   const ListRef& Lp = inf.l[0];
   const ListRef& Lc = inf.l[1];
   const ListRef& Ln = inf.l[2];
