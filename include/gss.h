@@ -112,6 +112,11 @@ int gss_engine_refresh(gss_engine* e);
 /* Engine::grad_hessian (engine.hpp:60; src/engine.cpp:220-242). */
 int gss_engine_grad_hessian(gss_engine* e, int64_t column, double* gradient,
                             double* hessian, double* fixed_term);
+/* Engine::grad_hessian_separated (engine.hpp:61; src/engine.cpp:244-329): the
+ * unfused path (materialised lanes, separate prefix / suffix scans, transform);
+ * the fusion ablation.  Same results as gss_engine_grad_hessian to ~1e-15. */
+int gss_engine_grad_hessian_separated(gss_engine* e, int64_t column, double* gradient,
+                                      double* hessian, double* fixed_term);
 /* Engine::log_likelihood (engine.hpp:63; src/engine.cpp:331-341). */
 int gss_engine_log_likelihood(gss_engine* e, double* out);
 

@@ -30,7 +30,7 @@ EXPORTS = [
     "gss_engine_get_ipcw", "gss_engine_counters", "gss_engine_fit",
     "gss_engine_max_abs_gradient", "gss_engine_last_timing", "gss_engine_grad_hessian_all",
     "gss_engine_cycle_stats", "gss_shard_aggregate", "gss_shard_sums",
-    "gss_engine_update_validate",
+    "gss_engine_update_validate", "gss_engine_grad_hessian_separated",
 ]
 
 
@@ -210,6 +210,13 @@ class Engine:
         g, h, f = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         check(lib().gss_engine_grad_hessian(self.h, ctypes.c_int64(j), ctypes.byref(g),
                                             ctypes.byref(h), ctypes.byref(f)))
+        return {"gradient": g.value, "hessian": h.value, "fixed_term": f.value}
+
+    def grad_hessian_separated(self, j):
+        """Engine::grad_hessian_separated (engine.hpp:61): the unfused path."""
+        g, h, f = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        check(lib().gss_engine_grad_hessian_separated(self.h, ctypes.c_int64(j), ctypes.byref(g),
+                                                      ctypes.byref(h), ctypes.byref(f)))
         return {"gradient": g.value, "hessian": h.value, "fixed_term": f.value}
 
     def log_likelihood(self):

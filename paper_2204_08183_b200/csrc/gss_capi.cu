@@ -147,6 +147,7 @@ struct gss_engine {
   uint8_t* penalized = nullptr;
   double *trec = nullptr, *tcar = nullptr, *cpay = nullptr, *slot_out = nullptr;
   double *ext = nullptr, *shard = nullptr;  // patient-shard carry in / aggregate out
+  double* sep = nullptr;                    // separated-path scratch (lazy)
   int32_t* slot_col = nullptr;
   int32_t* cta_tile0 = nullptr;
   unsigned int* bar = nullptr;
@@ -167,7 +168,7 @@ struct gss_engine {
     for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
                     (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
                     (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
-                    (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0})
+                    (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0, (void*)sep})
       if (q) cudaFree(q);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (ev0) cudaEventDestroy(ev0);
@@ -708,6 +709,14 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
     t0[E->grid] = nt;
     for (int k = 1; k <= E->grid; ++k)
       if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
+    if (std::getenv("GSS_VERBOSE")) {
+      for (int k = 0; k < E->grid; ++k) {
+        double wk = 0.0;
+        for (int t = t0[k]; t < t0[k + 1]; ++t) wk += w[t];
+        std::fprintf(stderr, "cta %d tiles [%d,%d) n=%d cost %.2f\n", k, t0[k], t0[k + 1],
+                     t0[k + 1] - t0[k], wk);
+      }
+    }
     EK(dalloc(&E->cta_tile0, E->grid + 1));
     EK(cudaMemcpy(E->cta_tile0, t0.data(), (E->grid + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
     P.cta_tile0 = E->cta_tile0;
@@ -829,6 +838,46 @@ int gss_engine_grad_hessian(gss_engine* E, int64_t column, double* gradient, dou
   if (gradient) *gradient = E->h_ctl->gradient;
   if (hessian) *hessian = E->h_ctl->hessian;
   if (fixed_term) *fixed_term = E->h_ctl->fixed_term;
+  return GSS_OK;
+}
+
+int gss_engine_grad_hessian_separated(gss_engine* E, int64_t column, double* gradient,
+                                      double* hessian, double* fixed_term) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (column < 0 || column >= E->ds->p)
+    return fail(GSS_ERR_INVALID_COLUMN, "grad_hessian: column " + std::to_string(column) +
+                                            " outside [0, " + std::to_string(E->ds->p) + ")");
+  cudaStream_t s = E->stream;
+  const size_t nsep = separated_scratch_doubles(E->ds->npad, E->ds->ntiles);
+  if (!E->sep) {
+    cudaError_t err = dalloc(&E->sep, nsep);
+    if (err != cudaSuccess) {
+      E->sep = nullptr;
+      return fail(err == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA,
+                  std::string("separated path scratch: ") + cudaGetErrorString(err));
+    }
+  }
+  GSS_CUDA(cudaMemsetAsync(E->dflag + 1, 0, sizeof(int), s));
+  double* out2 = E->sep + nsep - 2;
+  GSS_CUDA(launch_separated(E->prm, column, E->sep, E->dflag + 1, out2, s));
+  double sums[2] = {0.0, 0.0}, fixed = 0.0;
+  int bad = 0;
+  GSS_CUDA(cudaMemcpyAsync(sums, out2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaMemcpyAsync(&bad, E->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaMemcpyAsync(&fixed, E->fixed + column, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  if (bad)
+    return fail(GSS_ERR_NONPOS_DEN, "separated path: accumulated risk-set denominator <= 0");
+  // Engine::finish (src/engine.cpp:220-230)
+  const double g = fixed - sums[0];
+  double h = -sums[1];
+  if (h > 0.0) h = 0.0;
+  if (!std::isfinite(g) || !std::isfinite(h))
+    return fail(GSS_ERR_NONPOS_DEN, "derivatives overflowed; risk-set sums are not finite");
+  if (gradient) *gradient = g;
+  if (hessian) *hessian = h;
+  if (fixed_term) *fixed_term = fixed;
   return GSS_OK;
 }
 

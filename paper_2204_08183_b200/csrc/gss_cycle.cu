@@ -58,7 +58,7 @@ struct Geo {
   static constexpr int kGW = FG ? 8 : 4;  // warps per tile group (kPasses / kGW passes each)
   static_assert(kPasses % kGW == 0 && kW % kGW == 0, "group geometry");
   static constexpr int kNG = kW / kGW;    // tile groups (tiles in process at once)
-  static constexpr int kS = FG ? 4 : 7;   // ring stages
+  static constexpr int kS = FG ? 4 : 6;   // ring stages
   static constexpr int kCap = kNnzCap;    // per-list smem capacity (ints)
   static constexpr uint32_t kEBytes = kTileRows * 8;
   static constexpr uint32_t kCBytes = kTileRows * 4;
@@ -68,7 +68,8 @@ struct Geo {
   static constexpr uint32_t kOffG = kEBytes + kCBytes;
   static constexpr uint32_t kOffL = kEBytes + kCBytes + kGBytes;
   static constexpr uint32_t kStage = (kOffL + 3 * kLBytes + 1023) / 1024 * 1024;
-  static constexpr int kThreads = 32 * (kW + 1);
+  static constexpr int kP = 1;            // producer warps (independent issue chains)
+  static constexpr int kThreads = 32 * (kW + kP);
   static_assert(kStage % 1024 == 0, "stage alignment");
 };
 
@@ -79,7 +80,7 @@ struct ListRef {
 };
 
 struct StageInfo {
-  int tile, slot;
+  int tile, slot, li;  // li = tile index inside the CTA range
   ListRef l[3];  // 0 pending column, 1 scan column, 2 next column
 };
 
@@ -115,7 +116,26 @@ struct CcdState {
   double in_fixed, in_beta, in_hw, in_cmax;
   int in_pen, in_ind;
   SlotFields nf;
+  // phase profile (GSS_DEBUG & 256, one CTA): clock64 sums per phase
+  long long ph[12];
+  long long ph_t, ph_ref;
+  long long gfirst[4], glast[4];
+  int prev_rf, n_rf;
 };
+
+constexpr int kMaxTc = 64;  // tiles per CTA with shared-memory records / carries
+
+// lightweight phase profile (GSS_DEBUG bit 256) on thread 0 of CTA kProfCta
+constexpr int kProfCta = 5;
+#define PROF_ON (((P.dbg & 256) != 0) && cta == kProfCta)
+#define PROF_MARK(i)                                   \
+  do {                                                 \
+    if (PROF_ON && tid == 0) {                         \
+      const long long _n = clock64();                  \
+      cst.ph[i] += _n - cst.ph_t;                      \
+      cst.ph_t = _n;                                   \
+    }                                                  \
+  } while (0)
 
 template <bool FG>
 struct Tail {
@@ -143,7 +163,23 @@ struct Tail {
   int ext_f, ext_r;
   volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
   CcdState cs;
+  // per-tile records and in-range carries of the CTA's first kMaxTc tiles live
+  // in shared memory (tiles beyond use the global arrays); records are loaded
+  // from / flushed to global at launch start / end
+  double srec[kMaxTc][FG ? 12 : 6];
+  double scar[kMaxTc][FG ? 16 : 8];
 };
+
+template <bool FG>
+__device__ __forceinline__ double* rec_at(const CycleParams& P, Tail<FG>* tl, int t, int li) {
+  return li < kMaxTc ? tl->srec[li] : P.trec + size_t(t) * kRecStride;
+}
+template <bool FG>
+__device__ __forceinline__ double* car_at(const CycleParams& P, Tail<FG>* tl, int t, int li) {
+  return li < kMaxTc ? tl->scar[li] : P.tcar + size_t(t) * kCarStride;
+}
+// load through the right path (global fallback entries bypass L1)
+__device__ __forceinline__ double ld_rc(const double* p, int li) { return li < kMaxTc ? *p : __ldcg(p); }
 
 template <bool FG>
 __host__ __device__ constexpr size_t smem_total() {
@@ -246,7 +282,7 @@ __device__ __forceinline__ unsigned& trace_slot(int warp) {
 }
 // lane-0 only; no atomics: warp w of CTA 0 owns trace[w * kTrPerWarp ...]
 __device__ __forceinline__ void trace_ev(const CycleParams& P, int ev, int arg) {
-  if (!GSS_ENABLE_TRACE || !P.trace || blockIdx.x != 0) return;
+  if (!GSS_ENABLE_TRACE || !P.trace || blockIdx.x != 0 || (P.dbg & 32)) return;
   const int warp = threadIdx.x >> 5;
   unsigned& n = trace_slot(warp);
   const unsigned i = atomicAdd(&n, 1u);  // smem atomic: several lanes may trace
@@ -359,21 +395,25 @@ struct Ctx {
 template <bool FG>
 __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem, Tail<FG>* tl,
                                       int t0, int tc, const CUtensorMap* tm_e,
-                                      const CUtensorMap* tm_code, const CUtensorMap* tm_g) {
+                                      const CUtensorMap* tm_code, const CUtensorMap* tm_g,
+                                      int pw) {
   using G = Geo<FG>;
-  constexpr int S = G::kS;
+  constexpr int S = G::kS, NP = G::kP;
   const int lane = threadIdx.x & 31;
   // positions are 32-bit (slots x tiles-per-CTA < 2^31): no 64-bit divisions
   const unsigned total = static_cast<unsigned>(P.nslots) * static_cast<unsigned>(tc);
   const size_t nt1 = static_cast<size_t>(P.ntiles) + 1;
   const unsigned utc = static_cast<unsigned>(tc);
-  // waves of S positions; lane l < S owns position q0 + l (stage l of the wave)
-  for (unsigned q0 = 0; q0 < total; q0 += S) {
-    const unsigned qq = q0 + lane;
+  // producer warp pw owns positions q == pw (mod NP), in increasing order (the
+  // warps run independent latency chains); waves of 32 of its positions: lane
+  // l resolves position q0 + l*NP (list slices), then lane 0 waits the stages
+  // in order and lane l issues its position as soon as its stage is free
+  for (unsigned q0 = static_cast<unsigned>(pw); q0 < total; q0 += 32u * NP) {
+    const unsigned qq = q0 + static_cast<unsigned>(lane) * NP;
     long long lo[3] = {0, 0, 0};
     int cnt[3] = {0, 0, 0};
     int slot = 0, tloc = 0;
-    if (lane < S && qq < total) {
+    if (qq < total) {
       slot = static_cast<int>(qq / utc);
       tloc = static_cast<int>(qq - static_cast<unsigned>(slot) * utc);
       const int tile = t0 + tloc;
@@ -393,18 +433,15 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         }
       }
     }
-    const uint32_t phase = (q0 / S) & 1u;  // every position of the wave shares it
-    // lane 0 performs the waits in stage order (no lane-divergent mbarrier
-    // spinning inside the warp); lane i issues position q0+i as soon as its
-    // stage is free
-    for (int i = 0; i < S; ++i) {
-      if (q0 + i >= total) break;
+    for (int i = 0; i < 32; ++i) {
+      const unsigned qw = q0 + static_cast<unsigned>(i) * NP;
+      if (qw >= total) break;
+      const int s = static_cast<int>(qw % S);
       const int tl_i = __shfl_sync(0xffffffffu, tloc, i);
       if (lane == 0) {
-        const unsigned qw = q0 + i;
-        tl->mark[16 + i] = 0xA0u | (qw << 8);
+        tl->mark[16 + s] = 0xA0u | (qw << 8);
         trace_c0(P, 24, static_cast<int>(qw));
-        mbar_wait_wd(&tl->empty[i], phase ^ 1u, "producer empty-stage wait", qw, tl->mark);
+        mbar_wait_wd(&tl->empty[s], ((qw / S) & 1u) ^ 1u, "producer empty-stage wait", qw, tl->mark);
         trace_c0(P, 25, static_cast<int>(qw));
         // the same tile of the previous slot must have committed its pending
         // update (the committing group fenced generic -> async proxy before
@@ -425,12 +462,12 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
       __syncwarp();
       if (lane != i) continue;
       const int tile = t0 + tloc;
-      const int s = i;
       trace_c0(P, 23, static_cast<int>(qq));
       unsigned char* sb = smem + size_t(s) * G::kStage;
       StageInfo& inf = tl->info[s];
       inf.tile = tile;
       inf.slot = slot;
+      inf.li = tloc;
       uint32_t bytes = G::kEBytes + G::kCBytes + G::kGBytes;
       int32_t* lbase = reinterpret_cast<int32_t*>(sb + G::kOffL);
       uint32_t lbytes[3];
@@ -464,7 +501,6 @@ __device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem,
         if (lbytes[l])
           bulk_load_1d(lbase + l * G::kCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
       trace_c0(P, 26, static_cast<int>(qq));
-      tl->mark[16 + lane] = 0xD0u | (qq << 8);
     }
     __syncwarp();
   }
@@ -529,7 +565,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   const bool has_cur = KIND == kSlotGrad && ss.col >= 0;
 
   // ---- tile carries -> group smem (visible after the first group barrier) ----
-  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = __ldcg(P.tcar + size_t(t) * kCarStride + lane);
+  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
   const double* tcv = tl->gc[g];
 
   // ---- stale tile after a refresh: reload exp(eta) from global ----
@@ -809,7 +845,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   // ---- the next slot's per-tile record (from the patched staged tile) ----
   if constexpr (FUSED) {
     if (gw == 0 && lane == 0) {
-      double* rec = P.trec + size_t(t) * kRecStride;
+      double* rec = rec_at<FG>(P, tl, t, inf.li);
       rec[kRa] = ttot.v[0];
       rec[kRb] = ttot.v[NF];
       rec[kRc] = ttot.v[NF];
@@ -888,7 +924,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
 #pragma unroll
       for (int i = 0; i < NR; ++i) s[i] = __dadd_rn(s[i], tl->gr[g][w2][i]);
     }
-    double* rec = P.trec + size_t(t) * kRecStride;
+    double* rec = rec_at<FG>(P, tl, t, inf.li);
     rec[kRa] = ttot.v[0];
     rec[kRb] = s[0];
     rec[kRc] = s[1];
@@ -935,8 +971,8 @@ __device__ __forceinline__ bool consume_tile(const CycleParams& P, Tail<FG>* tl,
 // needed here: callers commit first.
 // ---------------------------------------------------------------------------
 template <bool FG>
-__device__ __noinline__ void records_from_global(const CycleParams& P, int t0, int tc, long long ncol,
-                                    int warp, int lane) {
+__device__ __noinline__ void records_from_global(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+                                                 long long ncol, int warp, int lane) {
   constexpr int W = Geo<FG>::kW;
   const size_t nt1 = size_t(P.ntiles) + 1;
   const bool n_ind = ncol >= 0 && (!P.has_vals || P.col_ind[ncol]);
@@ -981,15 +1017,17 @@ __device__ __noinline__ void records_from_global(const CycleParams& P, int t0, i
       ruc = warp_sum(ruc);
     }
     if (lane == 0) {
-      double* rec = P.trec + size_t(t) * kRecStride;
+      double* rec = rec_at<FG>(P, tl, t, i);
       rec[kRa] = a;
       rec[kRb] = rb;
       rec[kRc] = rc;
       rec[kRsa] = rec[kRsb] = rec[kRsc] = 0.0;
-      rec[kRua] = ua;
-      rec[kRub] = rub;
-      rec[kRuc] = ruc;
-      rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+      if constexpr (FG) {
+        rec[kRua] = ua;
+        rec[kRub] = rub;
+        rec[kRuc] = ruc;
+        rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+      }
     }
   }
 }
@@ -1000,8 +1038,9 @@ __device__ __noinline__ void records_from_global(const CycleParams& P, int t0, i
 // is a few ulps; load_beta()/refresh() API calls rebuild eta = X beta), and the
 // tile records are recomputed from the fresh values.  Returns max |eta|.
 template <bool FG>
-__device__ __noinline__ double refresh_tiles(const CycleParams& P, int t0, int tc, long long col, double delta,
-                                long long ncol, int warp, int lane) {
+__device__ __noinline__ double refresh_tiles(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+                                             long long col, double delta, long long ncol, int warp,
+                                             int lane) {
   constexpr int W = Geo<FG>::kW;
   const size_t nt1 = size_t(P.ntiles) + 1;
   const bool c_ind = !P.has_vals || P.col_ind[col];
@@ -1069,15 +1108,17 @@ __device__ __noinline__ double refresh_tiles(const CycleParams& P, int t0, int t
       ruc = warp_sum(ruc);
     }
     if (lane == 0) {
-      double* rec = P.trec + size_t(t) * kRecStride;
+      double* rec = rec_at<FG>(P, tl, t, i);
       rec[kRa] = a;
       rec[kRb] = rb;
       rec[kRc] = rc;
       rec[kRsa] = rec[kRsb] = rec[kRsc] = 0.0;
-      rec[kRua] = ua;
-      rec[kRub] = rub;
-      rec[kRuc] = ruc;
-      rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+      if constexpr (FG) {
+        rec[kRua] = ua;
+        rec[kRub] = rub;
+        rec[kRuc] = ruc;
+        rec[kRusa] = rec[kRusb] = rec[kRusc] = 0.0;
+      }
     }
   }
   return mx;
@@ -1086,8 +1127,9 @@ __device__ __noinline__ double refresh_tiles(const CycleParams& P, int t0, int t
 // Sparse correction of the records for a VALUED pending update (exp is not
 // linear in delta): rec += sum over the pending rows of (e_new - e_old) terms.
 template <bool FG>
-__device__ __noinline__ void correct_records_valued(const CycleParams& P, int t0, int tc, long long pcol,
-                                       double delta, long long ncol, int warp, int lane) {
+__device__ __noinline__ void correct_records_valued(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+                                                    long long pcol, double delta, long long ncol,
+                                                    int warp, int lane) {
   constexpr int W = Geo<FG>::kW;
   const size_t nt1 = size_t(P.ntiles) + 1;
   const bool n_ind = ncol >= 0 && (!P.has_vals || P.col_ind[ncol]);
@@ -1144,7 +1186,7 @@ __device__ __noinline__ void correct_records_valued(const CycleParams& P, int t0
       duc = warp_sum(duc);
     }
     if (lane == 0) {
-      double* rec = P.trec + size_t(t) * kRecStride;
+      double* rec = rec_at<FG>(P, tl, t, i);
       rec[kRa] = __dadd_rn(rec[kRa], da);
       rec[kRb] = __dadd_rn(rec[kRb], db);
       rec[kRc] = __dadd_rn(rec[kRc], dc);
@@ -1182,7 +1224,8 @@ __device__ __noinline__ int validate_rows(const CycleParams& P, int t0, int tc, 
 // (uncorrected value + s-part) and the CTA payload aggregates.
 // ---------------------------------------------------------------------------
 template <bool FG>
-__device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, double* pay, int lane) {
+__device__ __noinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, int t0, int tc, double* pay,
+                                        int lane) {
   // forward: exclusive segmented prefix, flags at stratum-first tiles
   double carry[6] = {0, 0, 0, 0, 0, 0};
   int seen = 0;  // a stratum-first tile was passed inside the range
@@ -1193,9 +1236,9 @@ __device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, do
     double v[6];
     int f = 0;
     if (valid) {
-      const double* rec = P.trec + size_t(t) * kRecStride;
+      const double* rec = rec_at<FG>(P, tl, t, i);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) v[k] = __ldcg(rec + k);
+      for (int k = 0; k < 6; ++k) v[k] = ld_rc(rec + k, i);
       f = P.tile_first[t] ? 1 : 0;
     } else {
 #pragma unroll
@@ -1239,7 +1282,7 @@ __device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, do
       for (int k = 0; k < 6; ++k) outv[k] = 0.0;
     }
     if (valid) {
-      double* tcp = P.tcar + size_t(t) * kCarStride;
+      double* tcp = car_at<FG>(P, tl, t, i);
 #pragma unroll
       for (int k = 0; k < 6; ++k) tcp[k] = outv[k];
       tcp[6] = reset ? 1.0 : 0.0;
@@ -1273,9 +1316,9 @@ __device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, do
       double v[6];
       int fnext = 0;  // tile i+1 (inside the range) starts a stratum
       if (valid) {
-        const double* rec = P.trec + size_t(t) * kRecStride;
+        const double* rec = rec_at<FG>(P, tl, t, i);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) v[k] = __ldcg(rec + 6 + k);
+        for (int k = 0; k < 6; ++k) v[k] = ld_rc(rec + 6 + k, i);
         fnext = (i + 1 < tc && P.tile_first[t + 1]) ? 1 : 0;
       } else {
 #pragma unroll
@@ -1305,7 +1348,7 @@ __device__ __noinline__ void range_scan(const CycleParams& P, int t0, int tc, do
       for (int k = 0; k < 6; ++k) outv[k] = sf ? s[k] : __dadd_rn(rc[k], s[k]);
       const int reset = sf | rseen;
       if (valid) {
-        double* tcp = P.tcar + size_t(t) * kCarStride;
+        double* tcp = car_at<FG>(P, tl, t, i);
 #pragma unroll
         for (int k = 0; k < 6; ++k) tcp[8 + k] = outv[k];
         tcp[14] = reset ? 1.0 : 0.0;
@@ -1459,7 +1502,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Tail<FG>* tl = reinterpret_cast<Tail<FG>*>(smem + size_t(S) * Gm::kStage);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cta = blockIdx.x;
+  const int cta = (P.dbg & 64) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x);
   const int G = P.grid;
   // static contiguous tile ranges, balanced by estimated tile cost (host,
   // per engine); P.cta_tile0[c] = first tile of CTA c, [G] = ntiles
@@ -1513,8 +1556,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     tl->ext_r = (P.ext && !fe) ? 1 : 0;
   }
 
-  if (warp == W) {
-    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g);
+  if (warp >= W) {
+    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g, warp - W);
     return;
   }
 
@@ -1530,6 +1573,12 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     cst.skipped = ctl->skipped;
     cst.err = ctl->err_code;
     cst.err_col = ctl->err_col;
+    for (int i = 0; i < 12; ++i) cst.ph[i] = 0;
+    for (int i = 0; i < 4; ++i) cst.gfirst[i] = cst.glast[i] = 0;
+    cst.ph_t = clock64();
+    cst.ph_ref = cst.ph_t;
+    cst.prev_rf = 0;
+    cst.n_rf = 0;
   }
   unsigned& bar_target = cst.bar_target;
   double& absmax = cst.absmax;
@@ -1555,6 +1604,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   auto exchange = [&]() {
     mark<FG>(tl, 0x20u | (static_cast<unsigned>(xi) << 8));
     consumer_sync(NC);
+    PROF_MARK(3);  // [3] range scan + publish
     if (tid == 0) {
       trace_cta(P, 31, xtr, 29);
       bar_target += static_cast<unsigned>(G);
@@ -1562,24 +1612,28 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       trace_cta(P, 32, xtr, 30);
       ++xtr;
     }
+    PROF_MARK(4);  // [4] grid barrier
     ++xi;
     consumer_sync(NC);
   };
   // publish this CTA's range aggregates (+ optional extras), exchange, gather
   auto publish_exchange_gather = [&](double p0, double p1, double pb) {
+    PROF_MARK(8);
     if (warp == 0) {
       double* pm = wbuf();
-      range_scan<FG>(P, t0, tc, pm, lane);
+      range_scan<FG>(P, tl, t0, tc, pm, lane);
       if (lane == 0) {
         pm[0] = p0;
         pm[1] = p1;
         pm[2] = pb;
       }
     }
+    PROF_MARK(9);
     exchange();
     if (tid == 0) trace_c0(P, 8, 0);
     gather_payloads<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, tid);
     if (tid == 0) trace_c0(P, 9, 0);
+    PROF_MARK(5);  // [5] gather
   };
 
   // slot fields of slot kk (thread 0; read by the consumers after a barrier)
@@ -1607,12 +1661,28 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     ss.fused = f.fused;
   };
   // ---- prologue: records for slot 0 and the slot-0 carries ----
-  if (!rec_ok) records_from_global<FG>(P, t0, tc, P.slot_col[0], warp, lane);
+  if (!rec_ok) {
+    records_from_global<FG>(P, tl, t0, tc, P.slot_col[0], warp, lane);
+  } else {  // records of the previous launch (global) -> shared memory
+    constexpr int R = FG ? 12 : 6;
+    const int nl = min(tc, kMaxTc);
+    for (int i = tid; i < nl * R; i += NC)
+      tl->srec[i / R][i % R] = __ldcg(P.trec + size_t(t0 + i / R) * kRecStride + i % R);
+  }
   __threadfence();
   consumer_sync(NC);
   publish_exchange_gather(0.0, 0.0, 0.0);
   if (P.shard_out && cta == 0 && warp == 0) shard_aggregate<FG>(P, rbuf(xi - 1), tl, lane);
+  // shared-memory records -> global (they outlive the launch)
+  auto flush_records = [&]() {
+    constexpr int R = FG ? 12 : 6;
+    consumer_sync(NC);
+    const int nl = min(tc, kMaxTc);
+    for (int i = tid; i < nl * R; i += NC)
+      P.trec[size_t(t0 + i / R) * kRecStride + i % R] = tl->srec[i / R][i % R];
+  };
   if (P.prologue_only) {
+    flush_records();
     if (tid == 0 && cta == 0) {
       ctl->bar_base = bar_target;
       ctl->rec_valid = err ? 0 : 1;  // the records serve the launch that follows
@@ -1672,6 +1742,13 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     int& in_pen = cst.in_pen;
     int& in_ind = cst.in_ind;
     SlotFields& nf = cst.nf;
+    if (PROF_ON && tid == 0 && cst.prev_rf) {  // refresh / valued tails counted apart
+      const long long _n = clock64();
+      cst.ph[7] += _n - cst.ph_t;
+      cst.ph_t = _n;
+      cst.ph_ref = _n;
+    }
+    PROF_MARK(0);  // [0] previous slot tail + loop top
     if (tid == 0) {
       in_ind = 1;
       if (col >= 0) {
@@ -1685,6 +1762,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       // the next slot's fields, resolved now (off the post-exchange critical path)
       nf = slot_fields(k + 1);
     }
+    PROF_MARK(1);  // [1] step-input loads on thread 0
     // ---- consume this CTA's tiles of slot k (warp per tile, fixed order) ----
     double acc0 = 0.0, acc1 = 0.0;
     int bad = 0;
@@ -1697,6 +1775,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       // pending update fence generic -> async proxy first (their stores were
       // issued in the patch phase and have drained by now, so this is cheap).
       for (int i = g; i < tc; i += NGr) {
+        if (PROF_ON && gw == 0 && lane == 0 && i == g && !cst.prev_rf)
+          cst.gfirst[g] += clock64() - cst.ph_ref;  // first tile start (rel. to the slot start)
         const unsigned q = static_cast<unsigned>(qbase) + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
         const uint32_t ph = (q / S) & 1u;
@@ -1718,6 +1798,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         }
       }
     }
+    if (PROF_ON && (warp % Gm::kGW) == 0 && lane == 0 && !cst.prev_rf) cst.glast[warp / Gm::kGW] += clock64() - cst.ph_ref;
     qbase += tc;
     acc0 = warp_sum(acc0);
     acc1 = warp_sum(acc1);
@@ -1728,6 +1809,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       tl->wpart[warp][2] = badw;
     }
     consumer_sync(NC);
+    PROF_MARK(2);  // [2] consumption (to the CTA barrier)
     if (tid == 0) {
       trace_c0(P, 3, k);
       trace_cta(P, 30, k);
@@ -1821,6 +1903,13 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       }
     }
     consumer_sync(NC);
+    PROF_MARK(6);  // [6] finish + step + carries
+    if (PROF_ON && tid == 0) {
+      cst.ph_ref = cst.ph_t;  // next slot's reference (before the barrier below)
+      cst.prev_rf = (tl->refresh || tl->valued || tl->need_exact) ? 1 : 0;
+      cst.n_rf += cst.prev_rf;
+    }
+    consumer_sync(NC);
     double delta = tl->bcast[3];
     // ---- exact validate-before-mutate (rare): one more exchange ----
     if (tl->need_exact) {
@@ -1850,7 +1939,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       delta = tl->bcast[3];
     }
     if (tl->refresh) {
-      const double mx = refresh_tiles<FG>(P, t0, tc, col, delta, ncol, warp, lane);
+      const double mx = refresh_tiles<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
       fence_proxy_async_global();
       double m = mx;
 #pragma unroll
@@ -1873,7 +1962,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         slack = 0.0;
       }
     } else if (tl->valued) {
-      correct_records_valued<FG>(P, t0, tc, col, delta, ncol, warp, lane);
+      correct_records_valued<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
       __threadfence();
       consumer_sync(NC);
       publish_exchange_gather(0.0, 0.0, 0.0);
@@ -1885,6 +1974,22 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     }
   }
 
+  if (PROF_ON && tid == 0) {
+    PROF_MARK(0);
+    const double ns = static_cast<double>(P.nslots - cst.n_rf);
+    printf("gss prof cta %d: %d refresh/valued/exact slots, their tails %.0f cycles each; publish: "
+           "pre %.0f range_scan %.0f (all exchanges)\n", cta,
+           cst.n_rf, cst.n_rf ? cst.ph[7] / static_cast<double>(cst.n_rf) : 0.0, cst.ph[8] / ns,
+           cst.ph[9] / ns);
+    printf("gss prof cta %d slots %d (cycles/slot): tail %.0f inputs %.0f consume %.0f publish %.0f "
+           "barrier %.0f gather %.0f step %.0f | group first-tile %.0f %.0f %.0f %.0f last %.0f %.0f "
+           "%.0f %.0f\n",
+           cta, P.nslots, cst.ph[0] / ns, cst.ph[1] / ns, cst.ph[2] / ns, cst.ph[3] / ns,
+           cst.ph[4] / ns, cst.ph[5] / ns, cst.ph[6] / ns, cst.gfirst[0] / ns, cst.gfirst[1] / ns,
+           cst.gfirst[2] / ns, cst.gfirst[3] / ns, cst.glast[0] / ns, cst.glast[1] / ns,
+           cst.glast[2] / ns, cst.glast[3] / ns);
+  }
+  flush_records();
   // ---- epilogue: CTA 0 persists the replicated state ----
   if (tid == 0 && cta == 0) {
     ctl->bar_base = bar_target;

@@ -119,6 +119,11 @@ cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,
 int cycle_max_grid(int device, bool weighted);
 size_t cycle_smem_bytes(bool weighted);
 
+// separated (unfused) derivative path (gss_separated.cu): out2 = (grad_sum, hess_sum)
+size_t separated_scratch_doubles(int64_t npad, int ntiles);
+cudaError_t launch_separated(const CycleParams& prm, int64_t column, double* scratch, int* bad,
+                             double* out2, cudaStream_t s);
+
 // aux (gss_aux.cu)
 cudaError_t launch_validate_csc(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                 int64_t n, int* bad, cudaStream_t s);

@@ -72,6 +72,13 @@ GradHess Engine::grad_hessian(std::size_t column) {
   return gh;
 }
 
+GradHess Engine::grad_hessian_separated(std::size_t column) {
+  GradHess gh;
+  check(gss_engine_grad_hessian_separated(h_, static_cast<int64_t>(column), &gh.gradient,
+                                          &gh.hessian, &gh.fixed_term));
+  return gh;
+}
+
 std::vector<GradHess> Engine::grad_hessian_all() {
   const std::size_t p = ds_->p();
   std::vector<double> g(p), h(p), f(p);

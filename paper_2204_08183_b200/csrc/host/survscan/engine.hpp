@@ -53,6 +53,8 @@ class Engine {
   void update_xbeta_sparse(std::size_t column, double delta);
   void refresh();
   GradHess grad_hessian(std::size_t column);
+  // unfused three-pass path (engine.hpp:61), the fusion ablation
+  GradHess grad_hessian_separated(std::size_t column);
   // all columns in one device launch (the batched sweep behind gamma_max)
   std::vector<GradHess> grad_hessian_all();
   double log_likelihood();

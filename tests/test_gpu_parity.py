@@ -258,3 +258,54 @@ def test_grad_hessian_all_matches_single(capi, model):
         # slot's per-tile records (another fixed summation order)
         assert rel_cond(allg["gradient"][j], gh["gradient"], gh["fixed_term"]) < 1e-13
         assert rel(allg["hessian"][j], gh["hessian"]) < 1e-13
+
+
+# ---- separated (unfused) path: Engine::grad_hessian_separated (engine.cpp:244-329) ----
+
+@pytest.mark.parametrize("model,n,p,quant,strata,valued,mask", [
+    ("cox", 80_000, 10, None, None, False, False),
+    ("cox", 70_001, 8, 40.0, 6, True, False),
+    ("cox", 50_000, 6, 20.0, None, False, True),
+    ("finegray", 60_000, 8, 30.0, None, False, False),
+    ("finegray", 45_000, 6, 25.0, 4, True, True),
+])
+def test_separated_equals_fused(capi, model, n, p, quant, strata, valued, mask):
+    """tests/test_engine.cpp:165-176 (and acceptance check 5): fused and
+    separated paths coincide to 1e-12; both match the oracle to 1e-10."""
+    ds = _random_sorted(n, p, 0.04, seed=5 * n + p, quant=quant, strata=strata, valued=valued,
+                        competing=0.5 if model == "finegray" else 0.0)
+    m = (np.random.default_rng(n).random(ds.n) < 0.8).astype(np.uint8) if mask else None
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), model, row_mask=m)
+    eng.load_beta(np.random.default_rng(9).uniform(-0.6, 0.6, size=p))
+    for j in range(p):
+        a, b = eng.grad_hessian(j), eng.grad_hessian_separated(j)
+        assert rel(a["gradient"], b["gradient"]) < 1e-12, j
+        assert rel(a["hessian"], b["hessian"]) < 1e-12, j
+        assert a["fixed_term"] == b["fixed_term"]
+
+
+def test_separated_known_answers_and_errors(capi):
+    """test_engine.cpp:48-61 (N=2 known answer through both paths) and :318
+    (InvalidColumnError from the separated path)."""
+    for name in cases("ka_"):
+        c = load(name)
+        ds = _sorted(c)
+        eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+        gh = eng.grad_hessian_separated(0)
+        assert gh["gradient"] == pytest.approx(float(c["grad0"][0]), abs=1e-15)
+        assert gh["hessian"] == pytest.approx(float(c["hess0"][0]), abs=1e-15)
+        with pytest.raises(capi.GssError) as ei:
+            eng.grad_hessian_separated(ds.p)
+        assert ei.value.kind == "InvalidColumnError"
+
+
+def test_separated_after_fit_tracks_updates(capi):
+    """After a device CCD fit (in-kernel updates and refreshes) the separated
+    path sees the same exp(eta) state as the fused one."""
+    ds = _random_sorted(40_000, 12, 0.05, seed=77, quant=50.0)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox", recompute_interval=5)
+    eng.fit(penalty="l1", strength=1.0, max_cycles=3)
+    for j in range(ds.p):
+        a, b = eng.grad_hessian(j), eng.grad_hessian_separated(j)
+        assert rel_cond(a["gradient"], b["gradient"], a["fixed_term"]) < 1e-12
+        assert rel(a["hessian"], b["hessian"]) < 1e-12
