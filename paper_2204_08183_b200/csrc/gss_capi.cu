@@ -599,7 +599,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(dalloc(&E->penalized, p));
   EK(dalloc(&E->trec, size_t(nt) * kRecStride));
   EK(dalloc(&E->tcar, size_t(nt) * kCarStride));
-  EK(dalloc(&E->cpay, size_t(2) * E->grid * kPayStride));
+  EK(dalloc(&E->cpay, size_t(2) * E->grid * (kPayStride + kPayAux)));
   EK(dalloc(&E->slot_out, size_t(p + 1) * 4));
   EK(dalloc(&E->slot_col, size_t(p + 1)));
   EK(dalloc(&E->bar, 1));

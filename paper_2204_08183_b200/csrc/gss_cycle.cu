@@ -69,7 +69,7 @@ struct Geo {
   static constexpr uint32_t kOffL = kEBytes + kCBytes + kGBytes;
   static constexpr uint32_t kStage = (kOffL + 3 * kLBytes + 1023) / 1024 * 1024;
   static constexpr int kP = 1;            // producer warps (independent issue chains)
-  static constexpr int kThreads = 32 * (kW + kP);
+  static constexpr int kThreads = 32 * (kW + 1 + kP);  // consumers, control warp, producer(s)
   static_assert(kStage % 1024 == 0, "stage alignment");
 };
 
@@ -121,9 +121,15 @@ struct CcdState {
   long long ph_t, ph_ref;
   long long gfirst[4], glast[4];
   int prev_rf, n_rf;
+  // control-warp loop state (shared memory is its home: no local-memory spills)
+  int xi, cstar, cend;
+  unsigned qbase;
+  long long to_refresh;
+  long long col, ncol;
 };
 
 constexpr int kMaxTc = 64;  // tiles per CTA with shared-memory records / carries
+constexpr int kMaxGrid = 148;  // CTAs (one per SM; B200)
 
 // lightweight phase profile (GSS_DEBUG bit 256) on thread 0 of CTA kProfCta
 constexpr int kProfCta = 5;
@@ -159,6 +165,10 @@ struct Tail {
   uint8_t cflag[256];   // CTA range holds a stratum-first tile (grid <= 256)
   int flag;
   int need_exact, refresh, valued;
+  int task;                  // consumer task handed out at the GO barrier
+  long long tcol, tncol;     // task parameters
+  double tdelta;
+  uint8_t tfirst[kMaxTc];    // tile_first of the CTA's first kMaxTc tiles
   int cstar, cend;
   int ext_f, ext_r;
   volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
@@ -166,6 +176,10 @@ struct Tail {
   // per-tile records and in-range carries of the CTA's first kMaxTc tiles live
   // in shared memory (tiles beyond use the global arrays); records are loaded
   // from / flushed to global at launch start / end
+  alignas(128) double gbuf[kMaxGrid][kPayStride];  // staged CTA payloads (gather)
+  uint64_t gbar;                                    // gather bulk-copy barrier
+  uint32_t gphase;
+  double gred[32][FG ? 15 : 9];                      // gather cross-lane partials
   double srec[kMaxTc][FG ? 12 : 6];
   double scar[kMaxTc][FG ? 16 : 8];
 };
@@ -184,6 +198,18 @@ __device__ __forceinline__ double ld_rc(const double* p, int li) { return li < k
 template <bool FG>
 __host__ __device__ constexpr size_t smem_total() {
   return 1024 + size_t(Geo<FG>::kS) * Geo<FG>::kStage + sizeof(Tail<FG>);
+}
+
+// consumer <-> control warp handshake (named barriers; 1 = consumers only,
+// 2.. = tile groups): consumers ARRIVE at kBarDone when their slot (or task) is
+// finished and SYNC at kBarGo; the control warp does the opposite
+constexpr int kBarDone = 8, kBarGo = 9;
+enum ConsumerTask : int { kTaskNext = 0, kTaskExit, kTaskExact, kTaskRefresh, kTaskValued };
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void consumer_sync(int nthreads) {
@@ -228,7 +254,7 @@ struct Step {
   double new_beta, applied, new_hw;
   bool skipped;
 };
-__device__ __noinline__ Step coordinate_step_dev(double beta_j, double grad, double hess, int kind,
+__device__ __forceinline__ Step coordinate_step_dev(double beta_j, double grad, double hess, int kind,
                                     double strength, bool penalized, double hw) {
   double geff = grad, heff = hess;
   bool at_zero_l1 = false;
@@ -353,15 +379,15 @@ __device__ __noinline__ void watchdog_trap(const char* what, unsigned a, unsigne
 // grid barrier over the co-resident CTAs (monotonic counter, no reset)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned target) {
-  __threadfence();
-  atomicAdd(bar, 1u);
+  // release-reduction: orders this thread's prior writes (the payload) before
+  // the arrival without a separate fence round trip
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
   const unsigned long long t0 = gtimer();
   unsigned it = 0;
   while (static_cast<int>(ld_acquire_u32(bar) - target) < 0) {
     if ((++it & 1023u) == 0 && gtimer() - t0 > 2 * kWatchdogNs)
       watchdog_trap("grid barrier", ld_acquire_u32(bar), target);
   }
-  __threadfence();
 }
 
 // bounded wait on an mbarrier phase (consumers: data landed)
@@ -393,7 +419,7 @@ struct Ctx {
 // producer: streams every (slot, tile) position of this CTA through the ring
 // ---------------------------------------------------------------------------
 template <bool FG>
-__device__ __noinline__ void producer(const CycleParams& P, unsigned char* smem, Tail<FG>* tl,
+__device__ __forceinline__ void producer(const CycleParams& P, unsigned char* smem, Tail<FG>* tl,
                                       int t0, int tc, const CUtensorMap* tm_e,
                                       const CUtensorMap* tm_code, const CUtensorMap* tm_g,
                                       int pw) {
@@ -1378,24 +1404,34 @@ __device__ __noinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, int 
   }
 }
 
-// All consumer threads read the published payloads once (thread c <- CTA c)
-// and reduce them with a fixed tree: the slot partials over all CTAs (the same
-// tree in every CTA => identical results everywhere), the fwd tails of CTAs
+// The control warp reads the published payloads (lane l <- CTAs l, l+32, ...)
+// and reduces them in a fixed order: the slot partials over all CTAs (the same
+// order in every CTA => identical results everywhere), the fwd tails of CTAs
 // [cstar, cta) and the rev heads of CTAs (cta, cend] (segmented by strata).
 // Result: tl->gs[0..2] partials, [3..8] fwd (a,b,c,sa,sb,sc), [9..14] rev.
 template <bool FG>
-__device__ __noinline__ void gather_payloads(const CycleParams& P, const double* pay_all, int cta, int cstar,
-                                int cend, Tail<FG>* tl, int tid) {
-  constexpr int W = Geo<FG>::kW, NC = 32 * W, NV = FG ? 15 : 9;
-  const int warp = tid >> 5, lane = tid & 31;
+__device__ __forceinline__ void gather_warp(const CycleParams& P, const double* pay_all, int cta,
+                                            int cstar, int cend, Tail<FG>* tl, int lane) {
+  constexpr int NV = FG ? 15 : 9;
   double v[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = 0.0;
-  for (int c = tid; c < P.grid; c += NC) {
-    const double* py = pay_all + size_t(c) * kPayStride;
-    double x[16];
-#pragma unroll
-    for (int i = 0; i < (FG ? 16 : 10); ++i) x[i] = __ldcg(py + i);
+  // every CTA's payload row in shared memory with ONE bulk copy (large
+  // transactions: the rows are read by all CTAs at once), then reduce there
+  const int G = P.grid;
+  const long long gt0 = clock64();
+  if (lane == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(G) * kPayStride * 8u;
+    fence_proxy_async_global();  // generic-proxy payload writes -> async-proxy read
+    mbar_arrive_expect_tx(&tl->gbar, bytes);
+    bulk_load_1d(&tl->gbuf[0][0], pay_all, bytes, &tl->gbar);
+  }
+  mbar_wait(&tl->gbar, tl->gphase);
+  __syncwarp();
+  if (lane == 0) tl->gphase ^= 1u;
+  const long long gt1 = clock64();
+  for (int c = lane; c < G; c += 32) {
+    const double* x = tl->gbuf[c];
     v[0] = __dadd_rn(v[0], x[0]);
     v[1] = __dadd_rn(v[1], x[1]);
     v[2] = __dadd_rn(v[2], x[2]);
@@ -1410,20 +1446,24 @@ __device__ __noinline__ void gather_payloads(const CycleParams& P, const double*
       }
     }
   }
+  const long long gt2 = clock64();
+  // cross-lane reduction through shared memory (fixed lane order; lane i sums value i)
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) tl->wred[warp][i] = v[i];
-  }
-  consumer_sync(NC);
-  if (tid < NV) {  // one thread per value, warps in fixed order
+  for (int i = 0; i < NV; ++i) tl->gred[lane][i] = v[i];
+  __syncwarp();
+  if (lane < NV) {
     double r = 0.0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) r = __dadd_rn(r, tl->wred[w][tid]);
-    tl->gs[tid] = r;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) r = __dadd_rn(r, tl->gred[l][lane]);
+    tl->gs[lane] = r;
   }
-  consumer_sync(NC);
+  __syncwarp();
+  const long long gt3 = clock64();
+  if (lane == 0 && (P.dbg & 256)) {
+    tl->cs.ph[6] += gt1 - gt0;
+    tl->cs.ph[7] += gt2 - gt1;
+    tl->cs.ph[8] += gt3 - gt2;
+  }
 }
 
 // corrected CTA carries from the gathered sums (thread 0)
@@ -1488,6 +1528,464 @@ __device__ void shard_aggregate(const CycleParams& P, const double* pall, const 
 }
 
 // ---------------------------------------------------------------------------
+// consumer side of the rare all-warp tasks (exact validation, refresh,
+// valued-update record correction): wait at GO, run the task, arrive at DONE,
+// until the control warp hands out NEXT (the next slot) or EXIT
+// ---------------------------------------------------------------------------
+template <bool FG>
+__device__ __forceinline__ void consumer_tasks(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+                                               int warp, int lane, int tid) {
+  constexpr int NC = 32 * Geo<FG>::kW, NB = NC + 32;
+  for (;;) {
+    bar_sync_n(kBarGo, NB);
+    const int task = *reinterpret_cast<volatile int*>(&tl->task);
+    if (task == kTaskNext || task == kTaskExit) return;
+    const long long col = tl->tcol, ncol = tl->tncol;
+    const double delta = tl->tdelta;
+    if (task == kTaskExact) {
+      if (validate_rows(P, t0, tc, col, delta, tid, NC)) tl->flag = 1;
+    } else if (task == kTaskRefresh) {
+      double m = refresh_tiles<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
+      fence_proxy_async_global();
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+      if (lane == 0) tl->wpart[warp][3] = m;
+      __threadfence();
+    } else if (task == kTaskValued) {
+      correct_records_valued<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
+      __threadfence();
+    }
+    __threadfence_block();
+    bar_arrive_n(kBarDone, NB);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the control warp: per slot, the in-range carry scan of the records as the
+// consumers release tiles, then (once the slot is consumed) the partial sums,
+// the grid exchange, the fixed-order gather, Engine::finish + coordinate_step
+// (replicated in every CTA) and the next slot's state.  Lane 0 runs the
+// serial parts; the warp runs the gathers and full range scans.
+// ---------------------------------------------------------------------------
+template <bool FG>
+__device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl, int cta, int t0,
+                                          int tc, int lane) {
+  using Gm = Geo<FG>;
+  constexpr int W = Gm::kW, NB = 32 * W + 32;
+  const int G = P.grid;
+  Ctl* ctl = P.ctl;
+  SlotState& ss = tl->ss;
+  const bool prof = (P.dbg & 256) && cta == kProfCta && lane == 0;
+  // phase profile in shared memory (no local-memory array)
+  long long* ph = tl->cs.ph;
+  if (lane == 0)
+    for (int i = 0; i < 12; ++i) ph[i] = 0;
+  tl->cs.ph_t = clock64();
+  auto pmark = [&](int i) {
+    if (prof) {
+      const long long n = clock64();
+      ph[i] += n - tl->cs.ph_t;
+      tl->cs.ph_t = n;
+    }
+  };
+  // replicated CCD state (identical in every CTA: same inputs, same order),
+  // kept in shared memory (written by lane 0)
+  CcdState& cs = tl->cs;
+  if (lane == 0) {
+    cs.bar_target = static_cast<unsigned>(ctl->bar_base);
+    cs.absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
+    cs.slack = ctl->bound_slack;
+    cs.accepted = ctl->accepted;
+    cs.refreshes = ctl->refreshes;
+    cs.skipped = ctl->skipped;
+    cs.err = ctl->err_code;
+    cs.err_col = ctl->err_col;
+    cs.xi = 0;
+    cs.qbase = 0;
+    // accepted updates until the next refresh (accepted % interval == 0)
+    cs.to_refresh = P.recompute_interval - (cs.accepted % P.recompute_interval);
+  }
+  __syncwarp();
+  unsigned& bar_target = cs.bar_target;
+  double& absmax = cs.absmax;
+  double& slack = cs.slack;
+  long long& accepted = cs.accepted;
+  long long& refreshes = cs.refreshes;
+  long long& skipped = cs.skipped;
+  int& err = cs.err;
+  long long& err_col = cs.err_col;
+  int& xi = cs.xi;  // payload double buffer, indexed by the exchange count
+  auto wbuf = [&]() { return P.cpay + (size_t(xi & 1) * G + cta) * kPayStride; };
+  auto rbuf = [&](int x) { return P.cpay + size_t(x & 1) * G * kPayStride; };
+  // auxiliary payload fields (rare paths)
+  auto waux = [&]() {
+    return P.cpay + size_t(2) * G * kPayStride + (size_t(xi & 1) * G + cta) * kPayAux;
+  };
+  auto raux = [&](int x) { return P.cpay + size_t(2) * G * kPayStride + size_t(x & 1) * G * kPayAux; };
+  // one gpu-scope fence + release by lane 0 (the cooperative-groups grid.sync pattern)
+  auto exchange = [&]() {
+    __syncwarp();
+    if (lane == 0) {
+      bar_target += static_cast<unsigned>(G);
+      grid_arrive_wait(P.bar, bar_target);
+      ++xi;
+    }
+    __syncwarp();
+  };
+  int& cstar = cs.cstar;
+  int& cend = cs.cend;
+  // full range scan of the records + publish + exchange + gather
+  auto publish_full = [&](double p0, double p1, double pb) {
+    double* pm = wbuf();
+    range_scan<FG>(P, tl, t0, tc, pm, lane);
+    if (lane == 0) {
+      pm[0] = p0;
+      pm[1] = p1;
+      pm[2] = pb;
+    }
+    exchange();
+    gather_warp<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, lane);
+  };
+  auto slot_fields = [&](int kk) {
+    SlotFields f{};
+    f.valid = kk < P.nslots;
+    if (!f.valid) return f;
+    const long long c = P.slot_col[kk];
+    const long long nc =
+        (kk + 1 < P.nslots) ? P.slot_col[kk + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
+    f.col = c;
+    f.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
+    f.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
+    f.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
+    f.fused = (!FG && P.mode == kModeCcd && c >= 0 && nc >= 0 && f.cind && f.nind &&
+               !(P.dbg & 8)) ? 1 : 0;
+    return f;
+  };
+  auto set_slot_fields = [&](const SlotFields& f) {
+    if (!f.valid) return;
+    ss.col = f.col;
+    ss.kind = f.kind;
+    ss.cind = f.cind;
+    ss.nind = f.nind;
+    ss.fused = f.fused;
+  };
+  auto go = [&](int task) {
+    if (lane == 0) tl->task = task;
+    __syncwarp();
+    bar_arrive_n(kBarGo, NB);
+  };
+  auto wait_done = [&]() { bar_sync_n(kBarDone, NB); };
+
+  // ---- prologue: records for slot 0 (consumers), then the slot-0 carries ----
+  wait_done();
+  if (lane == 0) {
+    cstar = tl->cstar;
+    cend = tl->cend;
+  }
+  __syncwarp();
+  publish_full(0.0, 0.0, 0.0);
+  if (P.shard_out && cta == 0) shard_aggregate<FG>(P, rbuf(xi - 1), tl, lane);
+  if (P.prologue_only) {
+    if (lane == 0 && cta == 0) {
+      ctl->bar_base = bar_target;
+      ctl->rec_valid = err ? 0 : 1;  // the records serve the launch that follows
+      ctl->rec_col = P.slot_col[0];
+    }
+    go(kTaskExit);
+    return;
+  }
+  if (lane == 0) {
+    set_carry_in<FG>(P, tl, 0.0);
+    ss.pcol = -1;
+    ss.delta = 0.0;
+    ss.phi = 1.0;
+    ss.pind = 1;
+    ss.refresh = 0;
+    ss.dry = err ? 1 : 0;
+    set_slot_fields(slot_fields(0));
+  }
+  go(kTaskNext);
+  pmark(5);
+
+  unsigned& qbase = cs.qbase;
+  for (int k = 0; k < P.nslots; ++k) {
+    // step inputs and the next slot's fields: loaded while the slot streams
+    long long& col = cs.col;
+    long long& ncol = cs.ncol;
+    double& in_fixed = cs.in_fixed;
+    double& in_beta = cs.in_beta;
+    double& in_hw = cs.in_hw;
+    double& in_cmax = cs.in_cmax;
+    int& in_pen = cs.in_pen;
+    int& in_ind = cs.in_ind;
+    SlotFields& nf = cs.nf;
+    if (lane == 0) {
+      in_ind = 1;
+      col = P.slot_col[k];
+      ncol = (k + 1 < P.nslots) ? P.slot_col[k + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
+      if (col >= 0) {
+        in_fixed = __ldcg(P.fixed + col);
+        in_beta = __ldcg(P.beta + col);
+        in_hw = __ldcg(P.halfwidth + col);
+        in_cmax = __ldcg(P.colmax + col);
+        in_pen = P.penalized[col];
+        in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
+      }
+      nf = slot_fields(k + 1);
+    }
+    // ---- in-range forward carry scan as the records appear (Cox) ----
+    if constexpr (!FG) {
+      if (lane == 0 && !(P.dbg & (16 | 512))) {
+        double car[6] = {0, 0, 0, 0, 0, 0};
+        int seen = 0;
+        const volatile unsigned* prog = tl->progress;
+        for (int i = 0; i < tc; ++i) {
+          const unsigned need = qbase + static_cast<unsigned>(i) + 1u;
+          const int g = i % Gm::kNG;
+          if (prog[g] < need) {
+            const unsigned long long tw = gtimer();
+            while (prog[g] < need) {
+              __nanosleep(64);
+              if (gtimer() - tw > kWatchdogNs) watchdog_trap("control record wait", need, prog[g]);
+            }
+          }
+          __threadfence_block();
+          const int t = t0 + i;
+          const double* rec = rec_at<FG>(P, tl, t, i);
+          const int f = (i < kMaxTc) ? tl->tfirst[i] : (P.tile_first[t] ? 1 : 0);
+          double* tcp = car_at<FG>(P, tl, t, i);
+#pragma unroll
+          for (int m = 0; m < 6; ++m) tcp[m] = f ? 0.0 : car[m];
+          tcp[6] = (seen | f) ? 1.0 : 0.0;
+#pragma unroll
+          for (int m = 0; m < 6; ++m) {
+            const double r = ld_rc(rec + m, i);
+            car[m] = f ? r : __dadd_rn(car[m], r);
+          }
+          seen |= f;
+        }
+        double* pm = wbuf();
+        pm[3] = seen ? 1.0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) pm[4 + m] = car[m];
+      }
+    }
+    wait_done();  // slot consumed: partials in wpart
+    pmark(0);
+    if (lane == 0) qbase += static_cast<unsigned>(tc);
+    __syncwarp();
+    if (P.dbg & 16) {  // ablation: stream only
+      go(kTaskNext);
+      continue;
+    }
+    double r0 = 0.0, r1 = 0.0, rb = 0.0;
+    if (lane == 0) {
+      for (int w = 0; w < W; ++w) {
+        r0 = __dadd_rn(r0, tl->wpart[w][0]);
+        r1 = __dadd_rn(r1, tl->wpart[w][1]);
+        rb = __dadd_rn(rb, tl->wpart[w][2]);
+      }
+    }
+    if (FG || (P.dbg & 512)) {
+      publish_full(r0, r1, rb);
+    } else {
+      if (lane == 0) {
+        double* pm = wbuf();
+        pm[0] = r0;
+        pm[1] = r1;
+        pm[2] = rb;
+      }
+      exchange();
+      pmark(1);
+      gather_warp<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, lane);
+    }
+    pmark(2);
+    // ---- finish + coordinate step (lane 0, replicated in every CTA) ----
+    double delta = 0.0, phi = 1.0, step_slack = 0.0;
+    int need_exact = 0, do_refresh = 0, valued = 0;
+    const bool dry = ss.dry != 0;
+    if (lane == 0) {
+      const double g0 = tl->gs[0], g1 = tl->gs[1];
+      const bool badden = tl->gs[2] != 0.0;
+      if (!dry) {
+        if (col < 0) {
+          const double ll = __dsub_rn(g0, g1);
+          if (badden && !err) {
+            err = kErrNonPos;
+            err_col = -1;
+          }
+          if (cta == 0) {
+            ctl->ll_fixed = g0;
+            ctl->ll_logden = g1;
+            ctl->loglik = ll;
+            if (P.slot_out) P.slot_out[size_t(k) * 4 + 3] = ll;
+          }
+        } else {
+          // Engine::finish (src/engine.cpp:220-230)
+          const double grad = __dsub_rn(in_fixed, g0);
+          double hess = -g1;
+          if (hess > 0.0) hess = 0.0;
+          const bool nonfinite = !isfinite(grad) || !isfinite(hess);
+          if (cta == 0) {
+            ctl->grad_sum = g0;
+            ctl->hess_sum = g1;
+            ctl->gradient = grad;
+            ctl->hessian = hess;
+            ctl->fixed_term = in_fixed;
+            if (P.slot_out) {
+              P.slot_out[size_t(k) * 4 + 0] = grad;
+              P.slot_out[size_t(k) * 4 + 1] = hess;
+              P.slot_out[size_t(k) * 4 + 2] = in_fixed;
+            }
+          }
+          if (badden || nonfinite) {
+            if (!err) {
+              err = kErrNonPos;
+              err_col = col;
+            }
+          } else if (P.mode == kModeCcd && !err) {
+            // coordinate_step + update decision (src/ccd.cpp:152-167)
+            const Step stp = coordinate_step_dev(in_beta, grad, hess, P.pen_kind, P.pen_strength,
+                                                 in_pen != 0, in_hw);
+            if (stp.skipped) {
+              ++skipped;
+            } else {
+              if (cta == 0) P.halfwidth[col] = stp.new_hw;
+              if (stp.applied != 0.0) {
+                step_slack = __dmul_rn(in_cmax, fabs(stp.applied));
+                delta = stp.applied;
+                // fast validate: max|eta| at the last refresh/load plus the
+                // accumulated |delta|*max|x| bounds every row
+                need_exact = (absmax + slack + step_slack <= kFastBound) ? 0 : 1;
+              }
+            }
+          }
+        }
+      }
+      phi = (delta != 0.0) ? exp(delta) : 1.0;
+      // carries for slot k+1 (linear path; refresh / valued paths redo them)
+      pmark(9);
+      set_carry_in<FG>(P, tl, __dsub_rn(phi, 1.0));
+      pmark(10);
+    }
+    need_exact = __shfl_sync(0xffffffffu, need_exact, 0);
+    pmark(11);
+    // ---- exact validate-before-mutate (rare): consumers check, one more exchange ----
+    if (need_exact) {
+      if (lane == 0) {
+        tl->flag = 0;
+        tl->tcol = col;
+        tl->tdelta = delta;
+      }
+      go(kTaskExact);
+      wait_done();
+      if (lane == 0) waux()[1] = tl->flag ? 1.0 : 0.0;
+      exchange();
+      if (lane == 0) {
+        const double* pa = raux(xi - 1);
+        bool any = false;
+        for (int c = 0; c < G; ++c) any |= __ldcg(pa + size_t(c) * kPayAux + 1) != 0.0;
+        if (any) {
+          if (!err) {
+            err = kErrOverflow;
+            err_col = col;
+          }
+          if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
+          delta = 0.0;
+          phi = 1.0;
+          set_carry_in<FG>(P, tl, 0.0);
+        }
+      }
+    }
+    // ---- accept: beta_[column] += delta, refresh cadence (src/engine.cpp:216-217) ----
+    if (lane == 0) {
+      if (delta != 0.0) {
+        if (cta == 0) P.beta[col] = __dadd_rn(in_beta, delta);
+        slack = __dadd_rn(slack, step_slack);
+        ++accepted;
+        if (--cs.to_refresh == 0) {
+          cs.to_refresh = P.recompute_interval;
+          do_refresh = 1;  // refresh subsumes the incremental update
+          ++refreshes;
+        }
+      }
+      valued = (delta != 0.0 && !do_refresh && !in_ind) ? 1 : 0;
+      tl->refresh = do_refresh;
+    }
+    do_refresh = __shfl_sync(0xffffffffu, do_refresh, 0);
+    pmark(4);
+    valued = __shfl_sync(0xffffffffu, valued, 0);
+    if (do_refresh) {
+      if (lane == 0) {
+        tl->tcol = col;
+        tl->tdelta = delta;
+        tl->tncol = ncol;
+      }
+      go(kTaskRefresh);
+      wait_done();
+      if (lane == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < W; ++w) mm = fmax(mm, tl->wpart[w][3]);
+        waux()[0] = mm;
+      }
+      publish_full(0.0, 0.0, 0.0);
+      if (lane == 0) {
+        set_carry_in<FG>(P, tl, 0.0);
+        const double* pa = raux(xi - 1);
+        double mm = 0.0;
+        for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayAux + 0));
+        absmax = mm;  // the bound is exact again
+        slack = 0.0;
+      }
+    } else if (valued) {
+      if (lane == 0) {
+        tl->tcol = col;
+        tl->tdelta = delta;
+        tl->tncol = ncol;
+      }
+      go(kTaskValued);
+      wait_done();
+      publish_full(0.0, 0.0, 0.0);
+      if (lane == 0) set_carry_in<FG>(P, tl, 0.0);
+    }
+    // ---- the next slot's pending update and fields ----
+    if (lane == 0) {
+      ss.pcol = (delta != 0.0 && !do_refresh) ? col : -1;
+      ss.delta = delta;
+      ss.phi = phi;
+      ss.pind = in_ind;
+      ss.refresh = do_refresh;
+      ss.dry = err ? 1 : 0;
+      set_slot_fields(nf);
+    }
+    pmark(3);
+    go(kTaskNext);
+  }
+
+  // ---- epilogue: CTA 0 persists the replicated state ----
+  if (lane == 0 && cta == 0) {
+    ctl->bar_base = bar_target;
+    ctl->eta_absmax_bits = static_cast<unsigned long long>(__double_as_longlong(absmax));
+    ctl->bound_slack = slack;
+    ctl->accepted = accepted;
+    ctl->refreshes = refreshes;
+    ctl->skipped = skipped;
+    ctl->err_code = err;
+    ctl->err_col = err_col;
+    ctl->rec_valid = (P.mode == kModeCcd && !err) ? 1 : 0;
+    ctl->rec_col = P.slot_col[0];
+  }
+  if (prof) {
+    const double ns = P.nslots > 0 ? static_cast<double>(P.nslots) : 1.0;
+    printf("gss prof cta %d slots %d (cycles/slot, control warp): consume %.0f publish+barrier %.0f "
+           "gather %.0f step+tasks %.0f (prologue %lld) | gather: wait %.0f sum %.0f reduce %.0f | "
+           "step %.0f carry %.0f shfl %.0f accept %.0f\n",
+           cta, P.nslots, ph[0] / ns, ph[1] / ns, ph[2] / ns, ph[3] / ns, ph[5], ph[6] / ns,
+           ph[7] / ns, ph[8] / ns, ph[9] / ns, ph[10] / ns, ph[11] / ns, ph[4] / ns);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // the persistent cycle kernel
 // ---------------------------------------------------------------------------
 template <bool FG>
@@ -1519,6 +2017,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       mbar_init(&tl->full[s], 1);
       mbar_init(&tl->empty[s], 1);
     }
+    mbar_init(&tl->gbar, 1);
+    tl->gphase = 0u;
     fence_mbar_init();
   }
   if (tid < Gm::kNG) tl->progress[tid] = 0u;
@@ -1527,6 +2027,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     (&tl->xm[0][0][0])[i] = 0u;
     (&tl->xn[0][0][0])[i] = 0u;
   }
+  for (int i = tid; i < min(tc, kMaxTc); i += blockDim.x) tl->tfirst[i] = P.tile_first[t0 + i];
+  if (tid == 0) tl->task = kTaskNext;
   // static stratum flags of every CTA range (carry segmentation bounds)
   for (int c = tid; c < G; c += blockDim.x) {
     uint8_t f = 0;
@@ -1556,111 +2058,22 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     tl->ext_r = (P.ext && !fe) ? 1 : 0;
   }
 
-  if (warp >= W) {
-    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g, warp - W);
+  if (warp > W) {
+    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g, warp - W - 1);
     return;
   }
-
-  // ------------------------- consumer / control warps ----------------------
-  // replicated CCD state (identical in every CTA: same inputs, same order)
-  CcdState& cst = tl->cs;
-  if (tid == 0) {
-    cst.bar_target = static_cast<unsigned>(ctl->bar_base);
-    cst.absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
-    cst.slack = ctl->bound_slack;
-    cst.accepted = ctl->accepted;
-    cst.refreshes = ctl->refreshes;
-    cst.skipped = ctl->skipped;
-    cst.err = ctl->err_code;
-    cst.err_col = ctl->err_col;
-    for (int i = 0; i < 12; ++i) cst.ph[i] = 0;
-    for (int i = 0; i < 4; ++i) cst.gfirst[i] = cst.glast[i] = 0;
-    cst.ph_t = clock64();
-    cst.ph_ref = cst.ph_t;
-    cst.prev_rf = 0;
-    cst.n_rf = 0;
-  }
-  unsigned& bar_target = cst.bar_target;
-  double& absmax = cst.absmax;
-  double& slack = cst.slack;
-  long long& accepted = cst.accepted;
-  long long& refreshes = cst.refreshes;
-  long long& skipped = cst.skipped;
-  int& err = cst.err;
-  long long& err_col = cst.err_col;
   const bool rec_ok = (P.mode == kModeCcd || P.reuse_records) && ctl->rec_valid &&
                       ctl->rec_col == P.slot_col[0];
   SlotState& ss = tl->ss;
-  consumer_sync(NC);
-  const int cstar = tl->cstar, cend = tl->cend;
+  if (warp == W) {
+    control_warp<FG>(P, tl, cta, t0, tc, lane);
+    return;
+  }
 
-  // payload double buffer, indexed by the exchange count
-  int xi = 0;
-  auto wbuf = [&]() { return P.cpay + (size_t(xi & 1) * G + cta) * kPayStride; };
-  auto rbuf = [&](int x) { return P.cpay + size_t(x & 1) * G * kPayStride; };
-  int xtr = 0;  // exchange ordinal (trace)
-  // CTA barrier first (orders every thread's writes before thread 0), then one
-  // gpu-scope fence + release by thread 0 (the cooperative-groups grid.sync pattern)
-  auto exchange = [&]() {
-    mark<FG>(tl, 0x20u | (static_cast<unsigned>(xi) << 8));
-    consumer_sync(NC);
-    PROF_MARK(3);  // [3] range scan + publish
-    if (tid == 0) {
-      trace_cta(P, 31, xtr, 29);
-      bar_target += static_cast<unsigned>(G);
-      grid_arrive_wait(P.bar, bar_target);
-      trace_cta(P, 32, xtr, 30);
-      ++xtr;
-    }
-    PROF_MARK(4);  // [4] grid barrier
-    ++xi;
-    consumer_sync(NC);
-  };
-  // publish this CTA's range aggregates (+ optional extras), exchange, gather
-  auto publish_exchange_gather = [&](double p0, double p1, double pb) {
-    PROF_MARK(8);
-    if (warp == 0) {
-      double* pm = wbuf();
-      range_scan<FG>(P, tl, t0, tc, pm, lane);
-      if (lane == 0) {
-        pm[0] = p0;
-        pm[1] = p1;
-        pm[2] = pb;
-      }
-    }
-    PROF_MARK(9);
-    exchange();
-    if (tid == 0) trace_c0(P, 8, 0);
-    gather_payloads<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, tid);
-    if (tid == 0) trace_c0(P, 9, 0);
-    PROF_MARK(5);  // [5] gather
-  };
-
-  // slot fields of slot kk (thread 0; read by the consumers after a barrier)
-  auto slot_fields = [&](int kk) {
-    SlotFields f{};
-    f.valid = kk < P.nslots;
-    if (!f.valid) return f;
-    const long long c = P.slot_col[kk];
-    const long long nc =
-        (kk + 1 < P.nslots) ? P.slot_col[kk + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
-    f.col = c;
-    f.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
-    f.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
-    f.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
-    f.fused = (!FG && P.mode == kModeCcd && c >= 0 && nc >= 0 && f.cind && f.nind &&
-               !(P.dbg & 8)) ? 1 : 0;
-    return f;
-  };
-  auto set_slot_fields = [&](const SlotFields& f) {
-    if (!f.valid) return;
-    ss.col = f.col;
-    ss.kind = f.kind;
-    ss.cind = f.cind;
-    ss.nind = f.nind;
-    ss.fused = f.fused;
-  };
-  // ---- prologue: records for slot 0 and the slot-0 carries ----
+  // ------------------------------ consumer warps ------------------------------
+  // Consumers only stream tiles and run the all-warp tasks the control warp
+  // hands them; every value that lives across slots is in shared memory
+  // (the control warp owns it), so nothing is spilled across the tile loop.
   if (!rec_ok) {
     records_from_global<FG>(P, tl, t0, tc, P.slot_col[0], warp, lane);
   } else {  // records of the previous launch (global) -> shared memory
@@ -1669,119 +2082,28 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     for (int i = tid; i < nl * R; i += NC)
       tl->srec[i / R][i % R] = __ldcg(P.trec + size_t(t0 + i / R) * kRecStride + i % R);
   }
-  __threadfence();
-  consumer_sync(NC);
-  publish_exchange_gather(0.0, 0.0, 0.0);
-  if (P.shard_out && cta == 0 && warp == 0) shard_aggregate<FG>(P, rbuf(xi - 1), tl, lane);
-  // shared-memory records -> global (they outlive the launch)
-  auto flush_records = [&]() {
-    constexpr int R = FG ? 12 : 6;
-    consumer_sync(NC);
-    const int nl = min(tc, kMaxTc);
-    for (int i = tid; i < nl * R; i += NC)
-      P.trec[size_t(t0 + i / R) * kRecStride + i % R] = tl->srec[i / R][i % R];
-  };
-  if (P.prologue_only) {
-    flush_records();
-    if (tid == 0 && cta == 0) {
-      ctl->bar_base = bar_target;
-      ctl->rec_valid = err ? 0 : 1;  // the records serve the launch that follows
-      ctl->rec_col = P.slot_col[0];
-    }
-    return;
-  }
-  if (tid == 0) {
-    set_carry_in<FG>(P, tl, 0.0);
-    ss.pcol = -1;
-    ss.delta = 0.0;
-    ss.phi = 1.0;
-    ss.pind = 1;
-    ss.refresh = 0;
-    ss.dry = err ? 1 : 0;
-    set_slot_fields(slot_fields(0));
-  }
-  consumer_sync(NC);
-
-  // accept the update: beta_[column] += delta, refresh cadence (src/engine.cpp:216-217)
-  auto accept = [&](double d, double bj, int ind, long long c) {
-    int do_refresh = 0;
-    if (d != 0.0) {
-      if (cta == 0) P.beta[c] = __dadd_rn(bj, d);
-      slack = __dadd_rn(slack, tl->bcast[5]);
-      ++accepted;
-      if (accepted % P.recompute_interval == 0) {
-        do_refresh = 1;  // refresh subsumes the incremental update
-        ++refreshes;
-      }
-    }
-    tl->refresh = do_refresh;
-    tl->valued = (d != 0.0 && !do_refresh && !ind) ? 1 : 0;
-  };
-  // the next slot's pending update and fields (thread 0)
-  auto finish_slot = [&](double d, double phi, int ind, long long c, const SlotFields& nf, int kk) {
-    ss.pcol = (d != 0.0 && !tl->refresh) ? c : -1;
-    ss.delta = d;
-    ss.phi = phi;
-    ss.pind = ind;
-    ss.refresh = tl->refresh;
-    ss.dry = err ? 1 : 0;
-    set_slot_fields(nf);
-    trace_c0(P, 5, kk);
-  };
-  long long qbase = 0;  // stream position of the slot's first tile
-  int gpar = 0;         // this warp's group: mask buffer of its next tile
-  for (int k = 0; k < P.nslots; ++k) {
-    const long long col = P.slot_col[k];
-    const long long ncol =
-        (k + 1 < P.nslots) ? P.slot_col[k + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
-    // step inputs, loaded now and used after the exchange (latency hidden)
-    double& in_fixed = cst.in_fixed;
-    double& in_beta = cst.in_beta;
-    double& in_hw = cst.in_hw;
-    double& in_cmax = cst.in_cmax;
-    int& in_pen = cst.in_pen;
-    int& in_ind = cst.in_ind;
-    SlotFields& nf = cst.nf;
-    if (PROF_ON && tid == 0 && cst.prev_rf) {  // refresh / valued tails counted apart
-      const long long _n = clock64();
-      cst.ph[7] += _n - cst.ph_t;
-      cst.ph_t = _n;
-      cst.ph_ref = _n;
-    }
-    PROF_MARK(0);  // [0] previous slot tail + loop top
-    if (tid == 0) {
-      in_ind = 1;
-      if (col >= 0) {
-        in_fixed = __ldcg(P.fixed + col);
-        in_beta = __ldcg(P.beta + col);
-        in_hw = __ldcg(P.halfwidth + col);
-        in_cmax = __ldcg(P.colmax + col);
-        in_pen = P.penalized[col];
-        in_ind = (!P.has_vals || P.col_ind[col]) ? 1 : 0;
-      }
-      // the next slot's fields, resolved now (off the post-exchange critical path)
-      nf = slot_fields(k + 1);
-    }
-    PROF_MARK(1);  // [1] step-input loads on thread 0
-    // ---- consume this CTA's tiles of slot k (warp per tile, fixed order) ----
+  __threadfence_block();
+  bar_arrive_n(kBarDone, NC + 32);
+  consumer_tasks<FG>(P, tl, t0, tc, warp, lane, tid);
+  unsigned qbase = 0;  // stream position of the slot's first tile
+  int gpar = 0;        // this warp's group: mask buffer of its next tile
+  const int nsl = (tl->task == kTaskExit) ? 0 : P.nslots;
+  for (int k = 0; k < nsl; ++k) {
     double acc0 = 0.0, acc1 = 0.0;
     int bad = 0;
     const bool dry = ss.dry != 0;
     {
       constexpr int NGr = Gm::kNG, GWr = Gm::kGW;
       const int g = warp / GWr, gw = warp % GWr;
-      // Progress (the producer's licence to reload a tile for the next slot)
-      // is published with the stage release; the threads that committed the
-      // pending update fence generic -> async proxy first (their stores were
-      // issued in the patch phase and have drained by now, so this is cheap).
+      // Progress (the producer's licence to reload a tile for the next slot,
+      // and the control warp's licence to read the tile's record) is
+      // published with the stage release; the threads that committed the
+      // pending update fence generic -> async proxy first.
       for (int i = g; i < tc; i += NGr) {
-        if (PROF_ON && gw == 0 && lane == 0 && i == g && !cst.prev_rf)
-          cst.gfirst[g] += clock64() - cst.ph_ref;  // first tile start (rel. to the slot start)
-        const unsigned q = static_cast<unsigned>(qbase) + static_cast<unsigned>(i);
+        const unsigned q = qbase + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
         const uint32_t ph = (q / S) & 1u;
         mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", q, lane == 0 ? tl->mark : nullptr);
-        if (gt0(warp, lane, GWr)) trace_c0(P, 21, static_cast<int>(q));
         unsigned char* sb = smem + size_t(s) * Gm::kStage;
         if (!dry && !(P.dbg & 1))
           consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1, bad,
@@ -1792,14 +2114,13 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         mark<FG>(tl, 0x15u | (q << 8));
         group_sync<FG>(g);
         if (gw == 0 && lane == 0) {
-          trace_c0(P, 22, static_cast<int>(q));
+          __threadfence_block();  // the tile's record before its progress
           *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = q + 1;
           mbar_arrive(&tl->empty[s]);
         }
       }
     }
-    if (PROF_ON && (warp % Gm::kGW) == 0 && lane == 0 && !cst.prev_rf) cst.glast[warp / Gm::kGW] += clock64() - cst.ph_ref;
-    qbase += tc;
+    qbase += static_cast<unsigned>(tc);
     acc0 = warp_sum(acc0);
     acc1 = warp_sum(acc1);
     const double badw = warp_sum(static_cast<double>(bad));
@@ -1808,200 +2129,17 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       tl->wpart[warp][1] = acc1;
       tl->wpart[warp][2] = badw;
     }
-    consumer_sync(NC);
-    PROF_MARK(2);  // [2] consumption (to the CTA barrier)
-    if (tid == 0) {
-      trace_c0(P, 3, k);
-      trace_cta(P, 30, k);
-    }
-    if (P.dbg & 16) continue;  // ablation: stream only
-    // ---- publish partials + range aggregates, exchange, gather ----
-    {
-      double r0 = 0.0, r1 = 0.0, rb = 0.0;
-      if (tid == 0) {
-        for (int w = 0; w < W; ++w) {
-          r0 = __dadd_rn(r0, tl->wpart[w][0]);
-          r1 = __dadd_rn(r1, tl->wpart[w][1]);
-          rb = __dadd_rn(rb, tl->wpart[w][2]);
-        }
-        trace_c0(P, 7, k);
-      }
-      publish_exchange_gather(r0, r1, rb);
-    }
-    if (tid == 0) trace_c0(P, 4, k);
-    // ---- finish + coordinate step (thread 0 of every CTA, replicated) ----
-    if (tid == 0) {
-      const double r0 = tl->gs[0], r1 = tl->gs[1];
-      const bool badden = tl->gs[2] != 0.0;
-      double delta = 0.0;
-      int need_exact = 0;
-      if (!dry) {
-        if (col < 0) {
-          const double ll = __dsub_rn(r0, r1);
-          if (badden && !err) {
-            err = kErrNonPos;
-            err_col = -1;
-          }
-          if (cta == 0) {
-            ctl->ll_fixed = r0;
-            ctl->ll_logden = r1;
-            ctl->loglik = ll;
-            if (P.slot_out) P.slot_out[size_t(k) * 4 + 3] = ll;
-          }
-        } else {
-          // Engine::finish (src/engine.cpp:220-230)
-          const double grad = __dsub_rn(in_fixed, r0);
-          double hess = -r1;
-          if (hess > 0.0) hess = 0.0;
-          const bool nonfinite = !isfinite(grad) || !isfinite(hess);
-          if (cta == 0) {
-            ctl->grad_sum = r0;
-            ctl->hess_sum = r1;
-            ctl->gradient = grad;
-            ctl->hessian = hess;
-            ctl->fixed_term = in_fixed;
-            if (P.slot_out) {
-              P.slot_out[size_t(k) * 4 + 0] = grad;
-              P.slot_out[size_t(k) * 4 + 1] = hess;
-              P.slot_out[size_t(k) * 4 + 2] = in_fixed;
-            }
-          }
-          if (badden || nonfinite) {
-            if (!err) {
-              err = kErrNonPos;
-              err_col = col;
-            }
-          } else if (P.mode == kModeCcd && !err) {
-            // coordinate_step + update decision (src/ccd.cpp:152-167)
-            const Step stp = coordinate_step_dev(in_beta, grad, hess, P.pen_kind, P.pen_strength,
-                                                 in_pen != 0, in_hw);
-            if (stp.skipped) {
-              ++skipped;
-            } else {
-              if (cta == 0) P.halfwidth[col] = stp.new_hw;
-              if (stp.applied != 0.0) {
-                const double step_slack = __dmul_rn(in_cmax, fabs(stp.applied));
-                delta = stp.applied;
-                // fast validate: max|eta| at the last refresh/load plus the
-                // accumulated |delta|*max|x| bounds every row
-                need_exact = (absmax + slack + step_slack <= kFastBound) ? 0 : 1;
-                tl->bcast[5] = step_slack;
-              }
-            }
-          }
-        }
-      }
-      tl->bcast[3] = delta;
-      tl->need_exact = need_exact;
-      const double phi = (delta != 0.0) ? exp(delta) : 1.0;
-      tl->bcast[6] = phi;
-      // carries for slot k+1 (linear path; refresh / valued paths redo them)
-      set_carry_in<FG>(P, tl, __dsub_rn(phi, 1.0));
-      if (!need_exact) {
-        accept(delta, in_beta, in_ind, col);
-        if (!tl->refresh && !tl->valued) finish_slot(delta, phi, in_ind, col, nf, k);
-      }
-    }
-    consumer_sync(NC);
-    PROF_MARK(6);  // [6] finish + step + carries
-    if (PROF_ON && tid == 0) {
-      cst.ph_ref = cst.ph_t;  // next slot's reference (before the barrier below)
-      cst.prev_rf = (tl->refresh || tl->valued || tl->need_exact) ? 1 : 0;
-      cst.n_rf += cst.prev_rf;
-    }
-    consumer_sync(NC);
-    double delta = tl->bcast[3];
-    // ---- exact validate-before-mutate (rare): one more exchange ----
-    if (tl->need_exact) {
-      if (tid == 0) tl->flag = 0;
-      consumer_sync(NC);
-      if (validate_rows(P, t0, tc, col, delta, tid, NC)) tl->flag = 1;
-      consumer_sync(NC);
-      if (tid == 0) wbuf()[17] = tl->flag ? 1.0 : 0.0;
-      exchange();
-      if (tid == 0) {
-        const double* pa = rbuf(xi - 1);
-        bool any = false;
-        for (int c = 0; c < G; ++c) any |= __ldcg(pa + size_t(c) * kPayStride + 17) != 0.0;
-        if (any) {
-          if (!err) {
-            err = kErrOverflow;
-            err_col = col;
-          }
-          if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
-          tl->bcast[3] = 0.0;
-        }
-        if (tl->bcast[3] == 0.0) tl->bcast[6] = 1.0;
-        accept(tl->bcast[3], in_beta, in_ind, col);
-        if (!tl->refresh && !tl->valued) finish_slot(tl->bcast[3], tl->bcast[6], in_ind, col, nf, k);
-      }
-      consumer_sync(NC);
-      delta = tl->bcast[3];
-    }
-    if (tl->refresh) {
-      const double mx = refresh_tiles<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
-      fence_proxy_async_global();
-      double m = mx;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
-      if (lane == 0) tl->wpart[warp][3] = m;
-      __threadfence();
-      consumer_sync(NC);
-      if (tid == 0) {
-        double mm = 0.0;
-        for (int w = 0; w < W; ++w) mm = fmax(mm, tl->wpart[w][3]);
-        wbuf()[16] = mm;
-      }
-      publish_exchange_gather(0.0, 0.0, 0.0);
-      if (tid == 0) {
-        set_carry_in<FG>(P, tl, 0.0);
-        const double* pa = rbuf(xi - 1);
-        double mm = 0.0;
-        for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayStride + 16));
-        absmax = mm;  // the bound is exact again
-        slack = 0.0;
-      }
-    } else if (tl->valued) {
-      correct_records_valued<FG>(P, tl, t0, tc, col, delta, ncol, warp, lane);
-      __threadfence();
-      consumer_sync(NC);
-      publish_exchange_gather(0.0, 0.0, 0.0);
-      if (tid == 0) set_carry_in<FG>(P, tl, 0.0);
-    }
-    if (tl->refresh || tl->valued) {
-      if (tid == 0) finish_slot(delta, tl->bcast[6], in_ind, col, nf, k);
-      consumer_sync(NC);
-    }
+    __threadfence_block();
+    bar_arrive_n(kBarDone, NC + 32);
+    consumer_tasks<FG>(P, tl, t0, tc, warp, lane, tid);
   }
-
-  if (PROF_ON && tid == 0) {
-    PROF_MARK(0);
-    const double ns = static_cast<double>(P.nslots - cst.n_rf);
-    printf("gss prof cta %d: %d refresh/valued/exact slots, their tails %.0f cycles each; publish: "
-           "pre %.0f range_scan %.0f (all exchanges)\n", cta,
-           cst.n_rf, cst.n_rf ? cst.ph[7] / static_cast<double>(cst.n_rf) : 0.0, cst.ph[8] / ns,
-           cst.ph[9] / ns);
-    printf("gss prof cta %d slots %d (cycles/slot): tail %.0f inputs %.0f consume %.0f publish %.0f "
-           "barrier %.0f gather %.0f step %.0f | group first-tile %.0f %.0f %.0f %.0f last %.0f %.0f "
-           "%.0f %.0f\n",
-           cta, P.nslots, cst.ph[0] / ns, cst.ph[1] / ns, cst.ph[2] / ns, cst.ph[3] / ns,
-           cst.ph[4] / ns, cst.ph[5] / ns, cst.ph[6] / ns, cst.gfirst[0] / ns, cst.gfirst[1] / ns,
-           cst.gfirst[2] / ns, cst.gfirst[3] / ns, cst.glast[0] / ns, cst.glast[1] / ns,
-           cst.glast[2] / ns, cst.glast[3] / ns);
-  }
-  flush_records();
-  // ---- epilogue: CTA 0 persists the replicated state ----
-  if (tid == 0 && cta == 0) {
-    ctl->bar_base = bar_target;
-    ctl->eta_absmax_bits = static_cast<unsigned long long>(__double_as_longlong(absmax));
-    ctl->bound_slack = slack;
-    ctl->accepted = accepted;
-    ctl->refreshes = refreshes;
-    ctl->skipped = skipped;
-    ctl->err_code = err;
-    ctl->err_col = err_col;
-    ctl->rec_valid = (P.mode == kModeCcd && !err) ? 1 : 0;
-    ctl->rec_col = P.slot_col[0];
+  // shared-memory records -> global (they outlive the launch)
+  {
+    constexpr int R = FG ? 12 : 6;
+    consumer_sync(NC);
+    const int nl = min(tc, kMaxTc);
+    for (int i = tid; i < nl * R; i += NC)
+      P.trec[size_t(t0 + i / R) * kRecStride + i % R] = tl->srec[i / R][i % R];
   }
 }
 
@@ -2025,7 +2163,7 @@ int cycle_max_grid(int device, bool weighted) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<false>, Geo<false>::kThreads,
                                                   smem_total<false>());
   }
-  return sms * (n > 0 ? 1 : 0);
+  return n > 0 ? (sms < kMaxGrid ? sms : kMaxGrid) : 0;
 }
 
 cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,

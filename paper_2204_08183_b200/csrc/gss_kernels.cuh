@@ -46,13 +46,16 @@ constexpr int kRecStride = 12;
 //   8..13 : rev segmented inclusive suffix inside the CTA range (ua,ub,uc,usa,usb,usc)
 //   14    : 1 if a stratum starts after this tile inside the range (no CTA carry-in)
 constexpr int kCarStride = 16;
-// CTA payload exchanged at the slot barrier
+// CTA payload exchanged at the slot barrier (one 128-byte row per CTA, gathered
+// with one bulk copy)
 //   0..2 : slot partials (p0, p1, bad)
 //   3    : 1 if any tile of the range starts a stratum
 //   4..9 : fwd tail  (tiles from the last stratum-first tile): a,b,c,sa,sb,sc
 //   10..15: rev head (tiles before the first stratum-first tile): ua,ub,uc,usa,usb,usc
-//   16   : max |eta| (refresh), 17: overflow flag (exact validation)
-constexpr int kPayStride = 24;
+// followed by the auxiliary rows [2][grid][kPayAux]: 0 max |eta| (refresh),
+// 1 overflow flag (exact validation)
+constexpr int kPayStride = 16;
+constexpr int kPayAux = 2;
 
 enum SlotKind : int { kSlotGrad = 0, kSlotLoglik = 1 };
 enum LaunchMode : int { kModeApi = 0, kModeCcd = 1 };
@@ -95,7 +98,7 @@ struct CycleParams {
   // ---- scratch ----
   double* trec;                // [ntiles][kRecStride]
   double* tcar;                // [ntiles][kCarStride]
-  double* cpay;                // [2][grid][kPayStride]
+  double* cpay;                // [2][grid][kPayStride] + [2][grid][kPayAux]
   unsigned int* bar;           // grid barrier counter
   Ctl* ctl;
   // optional event trace (GSS_TRACE=1): [cap][2] = (globaltimer ns, cta<<40|ev<<32|arg)
