@@ -997,7 +997,7 @@ __device__ __forceinline__ bool consume_tile(const CycleParams& P, Tail<FG>* tl,
 // needed here: callers commit first.
 // ---------------------------------------------------------------------------
 template <bool FG>
-__device__ __noinline__ void records_from_global(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+__device__ __forceinline__ void records_from_global(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
                                                  long long ncol, int warp, int lane) {
   constexpr int W = Geo<FG>::kW;
   const size_t nt1 = size_t(P.ntiles) + 1;
@@ -1064,7 +1064,7 @@ __device__ __noinline__ void records_from_global(const CycleParams& P, Tail<FG>*
 // is a few ulps; load_beta()/refresh() API calls rebuild eta = X beta), and the
 // tile records are recomputed from the fresh values.  Returns max |eta|.
 template <bool FG>
-__device__ __noinline__ double refresh_tiles(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+__device__ __forceinline__ double refresh_tiles(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
                                              long long col, double delta, long long ncol, int warp,
                                              int lane) {
   constexpr int W = Geo<FG>::kW;
@@ -1153,7 +1153,7 @@ __device__ __noinline__ double refresh_tiles(const CycleParams& P, Tail<FG>* tl,
 // Sparse correction of the records for a VALUED pending update (exp is not
 // linear in delta): rec += sum over the pending rows of (e_new - e_old) terms.
 template <bool FG>
-__device__ __noinline__ void correct_records_valued(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
+__device__ __forceinline__ void correct_records_valued(const CycleParams& P, Tail<FG>* tl, int t0, int tc,
                                                     long long pcol, double delta, long long ncol,
                                                     int warp, int lane) {
   constexpr int W = Geo<FG>::kW;
@@ -1228,7 +1228,7 @@ __device__ __noinline__ void correct_records_valued(const CycleParams& P, Tail<F
 }
 
 // Exact validate-before-mutate over this CTA's rows (src/engine.cpp:171-190).
-__device__ __noinline__ int validate_rows(const CycleParams& P, int t0, int tc, long long col, double delta,
+__device__ __forceinline__ int validate_rows(const CycleParams& P, int t0, int tc, long long col, double delta,
                              int tid, int nthr) {
   const size_t nt1 = size_t(P.ntiles) + 1;
   const long long cb = P.col_ptr[col];
@@ -1250,7 +1250,7 @@ __device__ __noinline__ int validate_rows(const CycleParams& P, int t0, int tc, 
 // (uncorrected value + s-part) and the CTA payload aggregates.
 // ---------------------------------------------------------------------------
 template <bool FG>
-__device__ __noinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, int t0, int tc, double* pay,
+__device__ __forceinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, int t0, int tc, double* pay,
                                         int lane) {
   // forward: exclusive segmented prefix, flags at stratum-first tiles
   double carry[6] = {0, 0, 0, 0, 0, 0};
