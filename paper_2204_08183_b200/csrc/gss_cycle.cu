@@ -1088,18 +1088,29 @@ __device__ __forceinline__ double refresh_tiles(const CycleParams& P, Tail<FG>* 
       __threadfence_block();
     }
     double a = 0.0, ua = 0.0;
-#pragma unroll 4
-    for (int k = lane; k < kTileRows; k += 32) {
-      const long long r = row0 + k;
-      const uint32_t cw = P.code[r];
-      if (cw & kCodeMasked) continue;
-      const double et = __ldcg(P.eta + r);
-      const double ev = exp(et);
-      P.e[r] = ev;
-      mx = fmax(mx, fabs(et));
-      a = __dadd_rn(a, ev);
+    // lane owns row pairs (2*lane + 64*j): 16-byte loads, 8 pairs in flight
+    // (masked / padding rows keep exp(eta) = 0)
+#pragma unroll 8
+    for (int j = 0; j < kTileRows / 64; ++j) {
+      const long long r = row0 + 2 * lane + 64 * j;
+      const uint2 cw = __ldcg(reinterpret_cast<const uint2*>(P.code + r));
+      const double2 et = __ldcg(reinterpret_cast<const double2*>(P.eta + r));
+      const bool m0 = (cw.x & kCodeMasked) != 0, m1 = (cw.y & kCodeMasked) != 0;
+      double2 ev;
+      ev.x = m0 ? 0.0 : exp(et.x);
+      ev.y = m1 ? 0.0 : exp(et.y);
+      *reinterpret_cast<double2*>(P.e + r) = ev;
+      if (!m0) {
+        mx = fmax(mx, fabs(et.x));
+        a = __dadd_rn(a, ev.x);
+      }
+      if (!m1) {
+        mx = fmax(mx, fabs(et.y));
+        a = __dadd_rn(a, ev.y);
+      }
       if constexpr (FG) {
-        if (cw & kCodeCompeting) ua = __dadd_rn(ua, __dmul_rn(__drcp_rn(P.g[r]), ev));
+        if (cw.x & kCodeCompeting) ua = __dadd_rn(ua, __dmul_rn(__drcp_rn(P.g[r]), ev.x));
+        if (cw.y & kCodeCompeting) ua = __dadd_rn(ua, __dmul_rn(__drcp_rn(P.g[r + 1]), ev.y));
       }
     }
     __syncwarp();
