@@ -128,7 +128,12 @@ struct CcdState {
   long long col, ncol;
 };
 
-constexpr int kMaxTc = 64;  // tiles per CTA with shared-memory records / carries
+// tiles per CTA with shared-memory records / carries (Fine-Gray: fewer, its
+// stages are larger)
+template <bool FG>
+struct MaxTc {
+  static constexpr int v = FG ? 40 : 64;
+};
 constexpr int kMaxGrid = 148;  // CTAs (one per SM; B200)
 
 // lightweight phase profile (GSS_DEBUG bit 256) on thread 0 of CTA kProfCta
@@ -160,7 +165,6 @@ struct Tail {
   unsigned int progress[NG];
   SlotState ss;
   double bcast[8];
-  double wred[W][16];
   double gs[16];
   uint8_t cflag[256];   // CTA range holds a stratum-first tile (grid <= 256)
   int flag;
@@ -168,7 +172,7 @@ struct Tail {
   int task;                  // consumer task handed out at the GO barrier
   long long tcol, tncol;     // task parameters
   double tdelta;
-  uint8_t tfirst[kMaxTc];    // tile_first of the CTA's first kMaxTc tiles
+  uint8_t tfirst[MaxTc<FG>::v];  // tile_first of the CTA's first MaxTc tiles
   int cstar, cend;
   int ext_f, ext_r;
   volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
@@ -180,20 +184,23 @@ struct Tail {
   uint64_t gbar;                                    // gather bulk-copy barrier
   uint32_t gphase;
   double gred[32][FG ? 15 : 9];                      // gather cross-lane partials
-  double srec[kMaxTc][FG ? 12 : 6];
-  double scar[kMaxTc][FG ? 16 : 8];
+  double srec[MaxTc<FG>::v][FG ? 12 : 6];
+  double scar[MaxTc<FG>::v][FG ? 16 : 8];
 };
 
 template <bool FG>
 __device__ __forceinline__ double* rec_at(const CycleParams& P, Tail<FG>* tl, int t, int li) {
-  return li < kMaxTc ? tl->srec[li] : P.trec + size_t(t) * kRecStride;
+  return li < MaxTc<FG>::v ? tl->srec[li] : P.trec + size_t(t) * kRecStride;
 }
 template <bool FG>
 __device__ __forceinline__ double* car_at(const CycleParams& P, Tail<FG>* tl, int t, int li) {
-  return li < kMaxTc ? tl->scar[li] : P.tcar + size_t(t) * kCarStride;
+  return li < MaxTc<FG>::v ? tl->scar[li] : P.tcar + size_t(t) * kCarStride;
 }
 // load through the right path (global fallback entries bypass L1)
-__device__ __forceinline__ double ld_rc(const double* p, int li) { return li < kMaxTc ? *p : __ldcg(p); }
+template <bool FG>
+__device__ __forceinline__ double ld_rc(const double* p, int li) {
+  return li < MaxTc<FG>::v ? *p : __ldcg(p);
+}
 
 template <bool FG>
 __host__ __device__ constexpr size_t smem_total() {
@@ -591,7 +598,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   const bool has_cur = KIND == kSlotGrad && ss.col >= 0;
 
   // ---- tile carries -> group smem (visible after the first group barrier) ----
-  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
+  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
   const double* tcv = tl->gc[g];
 
   // ---- stale tile after a refresh: reload exp(eta) from global ----
@@ -1275,7 +1282,7 @@ __device__ __forceinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, i
     if (valid) {
       const double* rec = rec_at<FG>(P, tl, t, i);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) v[k] = ld_rc(rec + k, i);
+      for (int k = 0; k < 6; ++k) v[k] = ld_rc<FG>(rec + k, i);
       f = P.tile_first[t] ? 1 : 0;
     } else {
 #pragma unroll
@@ -1355,7 +1362,7 @@ __device__ __forceinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, i
       if (valid) {
         const double* rec = rec_at<FG>(P, tl, t, i);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) v[k] = ld_rc(rec + 6 + k, i);
+        for (int k = 0; k < 6; ++k) v[k] = ld_rc<FG>(rec + 6 + k, i);
         fnext = (i + 1 < tc && P.tile_first[t + 1]) ? 1 : 0;
       } else {
 #pragma unroll
@@ -1763,14 +1770,14 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
           __threadfence_block();
           const int t = t0 + i;
           const double* rec = rec_at<FG>(P, tl, t, i);
-          const int f = (i < kMaxTc) ? tl->tfirst[i] : (P.tile_first[t] ? 1 : 0);
+          const int f = (i < MaxTc<FG>::v) ? tl->tfirst[i] : (P.tile_first[t] ? 1 : 0);
           double* tcp = car_at<FG>(P, tl, t, i);
 #pragma unroll
           for (int m = 0; m < 6; ++m) tcp[m] = f ? 0.0 : car[m];
           tcp[6] = (seen | f) ? 1.0 : 0.0;
 #pragma unroll
           for (int m = 0; m < 6; ++m) {
-            const double r = ld_rc(rec + m, i);
+            const double r = ld_rc<FG>(rec + m, i);
             car[m] = f ? r : __dadd_rn(car[m], r);
           }
           seen |= f;
@@ -2038,7 +2045,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     (&tl->xm[0][0][0])[i] = 0u;
     (&tl->xn[0][0][0])[i] = 0u;
   }
-  for (int i = tid; i < min(tc, kMaxTc); i += blockDim.x) tl->tfirst[i] = P.tile_first[t0 + i];
+  for (int i = tid; i < min(tc, MaxTc<FG>::v); i += blockDim.x) tl->tfirst[i] = P.tile_first[t0 + i];
   if (tid == 0) tl->task = kTaskNext;
   // static stratum flags of every CTA range (carry segmentation bounds)
   for (int c = tid; c < G; c += blockDim.x) {
@@ -2089,7 +2096,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     records_from_global<FG>(P, tl, t0, tc, P.slot_col[0], warp, lane);
   } else {  // records of the previous launch (global) -> shared memory
     constexpr int R = FG ? 12 : 6;
-    const int nl = min(tc, kMaxTc);
+    const int nl = min(tc, MaxTc<FG>::v);
     for (int i = tid; i < nl * R; i += NC)
       tl->srec[i / R][i % R] = __ldcg(P.trec + size_t(t0 + i / R) * kRecStride + i % R);
   }
@@ -2148,7 +2155,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   {
     constexpr int R = FG ? 12 : 6;
     consumer_sync(NC);
-    const int nl = min(tc, kMaxTc);
+    const int nl = min(tc, MaxTc<FG>::v);
     for (int i = tid; i < nl * R; i += NC)
       P.trec[size_t(t0 + i / R) * kRecStride + i % R] = tl->srec[i / R][i % R];
   }

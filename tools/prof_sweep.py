@@ -22,11 +22,13 @@ ap.add_argument("--cycles", type=int, default=2)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--strength", type=float, default=2 ** 0.5)
 ap.add_argument("--interval", type=int, default=100)
+ap.add_argument("--model", default="cox", choices=["cox", "finegray"])
 a = ap.parse_args()
 
-sim = capi.SimData(a.n, a.p, a.density, 0.8, 2, 0.9, 1000.0)
+sim = capi.SimData(a.n, a.p, a.density, 0.8, 2, 0.9, 1000.0,
+                   p_mix=0.5 if a.model == "finegray" else 0.0)
 ds = capi.Dataset(sim.times, sim.status, sim.col_ptr, sim.row_idx)
-eng = capi.Engine(ds, "cox", recompute_interval=a.interval)
+eng = capi.Engine(ds, a.model, recompute_interval=a.interval)
 if a.mode == "fit":
     t0 = time.perf_counter()
     r = eng.fit(penalty="l1", strength=a.strength, tol=1e-300, max_cycles=a.cycles)
