@@ -403,9 +403,10 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
                                              const volatile unsigned* marks = nullptr) {
   if (mbar_try_wait(bar, parity)) return;
   const unsigned long long t0 = gtimer();
+  unsigned it = 0;
   while (!mbar_try_wait(bar, parity)) {
     __nanosleep(64);  // back off: spinning waiters would steal the producer's issue slots
-    if (gtimer() - t0 > kWatchdogNs) watchdog_trap(what, info, parity, marks);
+    if ((++it & 63u) == 0 && gtimer() - t0 > kWatchdogNs) watchdog_trap(what, info, parity, marks);
   }
 }
 
@@ -1269,11 +1270,11 @@ __device__ __forceinline__ int validate_rows(const CycleParams& P, int t0, int t
 // ---------------------------------------------------------------------------
 template <bool FG>
 __device__ __forceinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, int t0, int tc, double* pay,
-                                        int lane) {
+                                        int lane, bool fwd = true) {
   // forward: exclusive segmented prefix, flags at stratum-first tiles
   double carry[6] = {0, 0, 0, 0, 0, 0};
   int seen = 0;  // a stratum-first tile was passed inside the range
-  for (int ch = 0; ch < tc; ch += 32) {
+  for (int ch = 0; fwd && ch < tc; ch += 32) {
     const int i = ch + lane;
     const bool valid = i < tc;
     const int t = t0 + i;
@@ -1341,7 +1342,7 @@ __device__ __forceinline__ void range_scan(const CycleParams& P, Tail<FG>* tl, i
     }
     seen |= tf;
   }
-  if (lane == 0) {
+  if (lane == 0 && fwd) {
     pay[3] = seen ? 1.0 : 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) pay[4 + k] = carry[k];
@@ -1751,9 +1752,10 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       }
       nf = slot_fields(k + 1);
     }
-    // ---- in-range forward carry scan as the records appear (Cox) ----
-    if constexpr (!FG) {
-      if (lane == 0 && !(P.dbg & (16 | 512))) {
+    // ---- in-range forward carry scan as the records appear (Cox; for
+    // Fine-Gray the full scan after the slot measured faster) ----
+    {
+      if (!FG && lane == 0 && !(P.dbg & (16 | 512))) {
         double car[6] = {0, 0, 0, 0, 0, 0};
         int seen = 0;
         const volatile unsigned* prog = tl->progress;
@@ -1762,9 +1764,11 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
           const int g = i % Gm::kNG;
           if (prog[g] < need) {
             const unsigned long long tw = gtimer();
+            unsigned it = 0;
             while (prog[g] < need) {
               __nanosleep(64);
-              if (gtimer() - tw > kWatchdogNs) watchdog_trap("control record wait", need, prog[g]);
+              if ((++it & 63u) == 0 && gtimer() - tw > kWatchdogNs)
+                watchdog_trap("control record wait", need, prog[g]);
             }
           }
           __threadfence_block();

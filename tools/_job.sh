@@ -1,3 +1,2 @@
-GSS_DEBUG=256 timeout 300 python tools/prof_sweep.py --n 10000000 --p 256 --mode fit --cycles 2 --model finegray 2>&1 | grep -v "^cycles" | tail -3 | cut -c1-400
-echo "== free-running"; GSS_DEBUG=16 timeout 300 python tools/prof_sweep.py --n 10000000 --p 256 --mode fit --cycles 2 --model finegray 2>&1 | tail -1
-echo "== tests"; timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+for d in 0 512; do GSS_DEBUG=$d timeout 300 python tools/prof_sweep.py --n 10000000 --p 256 --mode fit --cycles 2 --model finegray 2>&1 | tail -1; done
+timeout 300 python tools/prof_sweep.py --n 10000000 --p 512 --mode fit --cycles 3 2>&1 | tail -1
