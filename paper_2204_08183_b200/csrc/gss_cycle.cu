@@ -117,7 +117,7 @@ struct CcdState {
   int in_pen, in_ind;
   SlotFields nf;
   // phase profile (GSS_DEBUG & 256, one CTA): clock64 sums per phase
-  long long ph[12];
+  long long ph[16];
   long long ph_t, ph_ref;
   long long gfirst[4], glast[4];
   int prev_rf, n_rf;
@@ -1598,7 +1598,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   // phase profile in shared memory (no local-memory array)
   long long* ph = tl->cs.ph;
   if (lane == 0)
-    for (int i = 0; i < 12; ++i) ph[i] = 0;
+    for (int i = 0; i < 16; ++i) ph[i] = 0;
   tl->cs.ph_t = clock64();
   auto pmark = [&](int i) {
     if (prof) {
@@ -1943,8 +1943,11 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
         tl->tdelta = delta;
         tl->tncol = ncol;
       }
+      pmark(4);
       go(kTaskRefresh);
       wait_done();
+      pmark(12);
+      if (prof) ph[13] += 1;
       if (lane == 0) {
         double mm = 0.0;
         for (int w = 0; w < W; ++w) mm = fmax(mm, tl->wpart[w][3]);
@@ -2001,9 +2004,10 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     const double ns = P.nslots > 0 ? static_cast<double>(P.nslots) : 1.0;
     printf("gss prof cta %d slots %d (cycles/slot, control warp): consume %.0f publish+barrier %.0f "
            "gather %.0f step+tasks %.0f (prologue %lld) | gather: wait %.0f sum %.0f reduce %.0f | "
-           "step %.0f carry %.0f shfl %.0f accept %.0f\n",
+           "step %.0f carry %.0f shfl %.0f accept %.0f | refreshes %lld task %.0f\n",
            cta, P.nslots, ph[0] / ns, ph[1] / ns, ph[2] / ns, ph[3] / ns, ph[5], ph[6] / ns,
-           ph[7] / ns, ph[8] / ns, ph[9] / ns, ph[10] / ns, ph[11] / ns, ph[4] / ns);
+           ph[7] / ns, ph[8] / ns, ph[9] / ns, ph[10] / ns, ph[11] / ns, ph[4] / ns, ph[13],
+           ph[13] ? static_cast<double>(ph[12]) / ph[13] : 0.0);
   }
 }
 
