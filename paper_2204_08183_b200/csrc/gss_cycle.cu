@@ -170,6 +170,7 @@ struct Tail {
   int flag;
   int need_exact, refresh, valued;
   int task;                  // consumer task handed out at the GO barrier
+  unsigned issued;           // stream positions issued by the producer (in order)
   long long tcol, tncol;     // task parameters
   double tdelta;
   uint8_t tfirst[MaxTc<FG>::v];  // tile_first of the CTA's first MaxTc tiles
@@ -535,6 +536,9 @@ __device__ __forceinline__ void producer(const CycleParams& P, unsigned char* sm
         if (lbytes[l])
           bulk_load_1d(lbase + l * G::kCap, P.row_idx + (lo[l] & ~3LL), lbytes[l], &tl->full[s]);
       trace_c0(P, 26, static_cast<int>(qq));
+      // positions are issued in order: publish the count (consumers check it
+      // before their parity wait, see the consumer loop)
+      *reinterpret_cast<volatile unsigned*>(&tl->issued) = qq + 1;
     }
     __syncwarp();
   }
@@ -2045,6 +2049,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     }
     mbar_init(&tl->gbar, 1);
     tl->gphase = 0u;
+    tl->issued = 0u;
     fence_mbar_init();
   }
   if (tid < Gm::kNG) tl->progress[tid] = 0u;
@@ -2129,6 +2134,23 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         const unsigned q = qbase + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
         const uint32_t ph = (q / S) & 1u;
+        // A parity wait only tells apart consecutive phases of a stage: a group
+        // that runs two ring cycles ahead of a slow group would see the phase
+        // of position q - 2S as "complete". Wait until the producer has issued
+        // q (it issues q only after q - S was released), then the parity test
+        // is exact.
+        {
+          const volatile unsigned* iss = &tl->issued;
+          if (*iss <= q) {
+            const unsigned long long tw = gtimer();
+            unsigned it = 0;
+            while (*iss <= q) {
+              __nanosleep(32);
+              if ((++it & 63u) == 0 && gtimer() - tw > kWatchdogNs)
+                watchdog_trap("consumer issue wait", q, *iss, lane == 0 ? tl->mark : nullptr);
+            }
+          }
+        }
         mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", q, lane == 0 ? tl->mark : nullptr);
         unsigned char* sb = smem + size_t(s) * Gm::kStage;
         if (!dry && !(P.dbg & 1))
