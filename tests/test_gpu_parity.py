@@ -309,3 +309,45 @@ def test_separated_after_fit_tracks_updates(capi):
         a, b = eng.grad_hessian(j), eng.grad_hessian_separated(j)
         assert rel_cond(a["gradient"], b["gradient"], a["fixed_term"]) < 1e-12
         assert rel(a["hessian"], b["hessian"]) < 1e-12
+
+
+def test_exact_overflow_validation_path_vs_oracle(capi):
+    """One extreme value per column (|x| = 1000, on a censored row with the
+    smallest time, so it sits in no event's risk set and leaves beta at the
+    bulk's scale) makes the fast |x'beta| bound (max|eta| + sum |delta| *
+    max|x|) pass 700 after a few updates: the kernel takes the exact
+    validate-before-mutate path (src/engine.cpp:171-190: consumers check every
+    touched row, one extra grid exchange) on most coordinates. Results must
+    still match the oracle."""
+    rng = np.random.default_rng(404)
+    n, p = 40_000, 8
+    t = rng.exponential(size=n)
+    status = (rng.random(n) < 0.7).astype(np.int64)
+    outl = np.argsort(t)[:p]  # smallest times
+    status[outl] = 0
+    bulk = np.setdiff1d(np.arange(n), outl)
+    rows, cols, vals = [], [], []
+    eta = np.zeros(n)
+    for j in range(p):
+        r = rng.choice(bulk, size=2000, replace=False)
+        v = np.round(rng.uniform(-3.0, 3.0, size=r.size), 2)
+        v[v == 0] = 1.5
+        eta[r] += 0.3 * v
+        r = np.append(r, outl[j])
+        v = np.append(v, 1000.0)
+        o = np.argsort(r)
+        rows.append(r[o])
+        cols.append(np.full(r.size, j))
+        vals.append(v[o])
+    t = t / np.exp(eta)
+    t[outl] = t.min() / 2.0 - np.arange(p) * 1e-9  # keep them last in time
+    t = np.ceil(t * 1e6) / 1e6
+    ds = orc.assemble(t, status, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p)
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
+    ref = orc.OracleEngine(ds, "cox")
+    r1 = eng.fit(penalty="l1", strength=1.0, max_cycles=6)
+    r2 = ref.fit(penalty="l1", strength=1.0, max_cycles=6)
+    assert r1["cycles"] == r2["cycles"]
+    assert np.max(rel(r1["beta"], r2["beta"])) < TOL_BETA
+    assert np.max(rel(r1["objective_trace"], r2["objective_trace"])) < TOL_DERIV
+    assert np.abs(r1["beta"]).sum() * 1000.0 > 700.0  # the fast bound was exceeded
