@@ -626,7 +626,11 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
         P.eta[r] = ne;
       }
       *pe = en;
-      P.e[r] = en;
+      if constexpr (FG)  // L2 atomic store: measured 2% faster for Fine-Gray, not for Cox
+        atomicExch(reinterpret_cast<unsigned long long*>(P.e + r),
+                   static_cast<unsigned long long>(__double_as_longlong(en)));
+      else
+        P.e[r] = en;
     }
   }
   // ---- scan-column bitmask per thread-row (xm is all-zero on entry) ----
