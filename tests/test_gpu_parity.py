@@ -351,3 +351,41 @@ def test_exact_overflow_validation_path_vs_oracle(capi):
     assert np.max(rel(r1["beta"], r2["beta"])) < TOL_BETA
     assert np.max(rel(r1["objective_trace"], r2["objective_trace"])) < TOL_DERIV
     assert np.abs(r1["beta"]).sum() * 1000.0 > 700.0  # the fast bound was exceeded
+
+
+def test_fit_overflow_mid_cycle_raises_like_reference(capi):
+    """An accepted step that would push some |x'beta| past 700 raises
+    OverflowError from fit (validate-before-mutate, src/engine.cpp:171-190);
+    on the device the error is raised inside the cycle kernel, which then
+    streams the rest of the cycle without work ('dry') and must end cleanly.
+    The extreme value sits on a censored row with the smallest time (in no
+    event's risk set), so beta follows the bulk and 1e5 * beta overflows."""
+    rng = np.random.default_rng(77)
+    n, p = 30_000, 6
+    t = rng.exponential(size=n)
+    status = (rng.random(n) < 0.7).astype(np.int64)
+    last = int(np.argmin(t))
+    status[last] = 0
+    bulk = np.setdiff1d(np.arange(n), [last])
+    rows, cols, vals = [], [], []
+    eta = np.zeros(n)
+    for j in range(p):
+        r = rng.choice(bulk, size=1500, replace=False)
+        v = np.round(rng.uniform(-3.0, 3.0, size=r.size), 2)
+        v[v == 0] = 1.5
+        eta[r] += 0.4 * v
+        r = np.append(r, last)
+        v = np.append(v, 1.0e5)
+        o = np.argsort(r)
+        rows.append(r[o])
+        cols.append(np.full(r.size, j))
+        vals.append(v[o])
+    t = t / np.exp(eta)
+    t[last] = t.min() / 2.0
+    ds = orc.assemble(t, status, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p)
+    with pytest.raises(orc.OracleError) as e_ref:
+        orc.OracleEngine(ds, "cox").fit(penalty="none", max_cycles=5)
+    with pytest.raises(capi.GssError) as e_dev:
+        capi.Engine(capi.Dataset.from_sorted(ds), "cox").fit(penalty="none", max_cycles=5)
+    assert e_ref.value.kind == "OverflowError"
+    assert e_dev.value.kind == "OverflowError"
