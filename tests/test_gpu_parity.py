@@ -353,7 +353,8 @@ def test_exact_overflow_validation_path_vs_oracle(capi):
     assert np.abs(r1["beta"]).sum() * 1000.0 > 700.0  # the fast bound was exceeded
 
 
-def test_fit_overflow_mid_cycle_raises_like_reference(capi):
+@pytest.mark.parametrize("model", ["cox", "finegray"])
+def test_fit_overflow_mid_cycle_raises_like_reference(capi, model):
     """An accepted step that would push some |x'beta| past 700 raises
     OverflowError from fit (validate-before-mutate, src/engine.cpp:171-190);
     on the device the error is raised inside the cycle kernel, which then
@@ -364,6 +365,8 @@ def test_fit_overflow_mid_cycle_raises_like_reference(capi):
     n, p = 30_000, 6
     t = rng.exponential(size=n)
     status = (rng.random(n) < 0.7).astype(np.int64)
+    if model == "finegray":  # competing rows: the weighted (forward-backward) kernel
+        status[(status == 0) & (rng.random(n) < 0.5)] = 2
     last = int(np.argmin(t))
     status[last] = 0
     bulk = np.setdiff1d(np.arange(n), [last])
@@ -384,8 +387,8 @@ def test_fit_overflow_mid_cycle_raises_like_reference(capi):
     t[last] = t.min() / 2.0
     ds = orc.assemble(t, status, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p)
     with pytest.raises(orc.OracleError) as e_ref:
-        orc.OracleEngine(ds, "cox").fit(penalty="none", max_cycles=5)
+        orc.OracleEngine(ds, model).fit(penalty="none", max_cycles=5)
     with pytest.raises(capi.GssError) as e_dev:
-        capi.Engine(capi.Dataset.from_sorted(ds), "cox").fit(penalty="none", max_cycles=5)
+        capi.Engine(capi.Dataset.from_sorted(ds), model).fit(penalty="none", max_cycles=5)
     assert e_ref.value.kind == "OverflowError"
     assert e_dev.value.kind == "OverflowError"
