@@ -311,7 +311,8 @@ def test_separated_after_fit_tracks_updates(capi):
         assert rel(a["hessian"], b["hessian"]) < 1e-12
 
 
-def test_exact_overflow_validation_path_vs_oracle(capi):
+@pytest.mark.parametrize("model", ["cox", "finegray"])
+def test_exact_overflow_validation_path_vs_oracle(capi, model):
     """One extreme value per column (|x| = 1000, on a censored row with the
     smallest time, so it sits in no event's risk set and leaves beta at the
     bulk's scale) makes the fast |x'beta| bound (max|eta| + sum |delta| *
@@ -323,6 +324,8 @@ def test_exact_overflow_validation_path_vs_oracle(capi):
     n, p = 40_000, 8
     t = rng.exponential(size=n)
     status = (rng.random(n) < 0.7).astype(np.int64)
+    if model == "finegray":  # competing rows: the weighted (forward-backward) kernel
+        status[(status == 0) & (rng.random(n) < 0.5)] = 2
     outl = np.argsort(t)[:p]  # smallest times
     status[outl] = 0
     bulk = np.setdiff1d(np.arange(n), outl)
@@ -343,8 +346,8 @@ def test_exact_overflow_validation_path_vs_oracle(capi):
     t[outl] = t.min() / 2.0 - np.arange(p) * 1e-9  # keep them last in time
     t = np.ceil(t * 1e6) / 1e6
     ds = orc.assemble(t, status, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p)
-    eng = capi.Engine(capi.Dataset.from_sorted(ds), "cox")
-    ref = orc.OracleEngine(ds, "cox")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), model)
+    ref = orc.OracleEngine(ds, model)
     r1 = eng.fit(penalty="l1", strength=1.0, max_cycles=6)
     r2 = ref.fit(penalty="l1", strength=1.0, max_cycles=6)
     assert r1["cycles"] == r2["cycles"]
