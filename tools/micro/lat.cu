@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/lat tools/micro/lat.cu
 // Latency microbenchmark: dependent chains of fp64 ops, shuffles, smem loads
 // on one warp (clock64), with and without 16 other busy warps on the SM.
 #include <cstdio>

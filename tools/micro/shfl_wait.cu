@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/shfl_wait tools/micro/shfl_wait.cu
 // Does a warp parked in mbarrier.try_wait slow other warps' shuffles / smem ops?
 #include <cstdio>
 #include <cstdint>
