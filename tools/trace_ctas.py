@@ -1,4 +1,8 @@
-"""Per-CTA slot timing of the cycle kernel (trace build, all CTAs, no CTA-0
+"""(Historical: written for the kernel before the control-warp restructure;
+several events it reads are no longer emitted. The current per-phase
+profile is GSS_DEBUG=256 / 1024 with tools/prof_sweep.py.)
+
+Per-CTA slot timing of the cycle kernel (trace build, all CTAs, no CTA-0
 event trace): how much of each coordinate is spent waiting for the slowest
 CTA, and whether the same CTAs are slow every slot (static imbalance) or not.
 

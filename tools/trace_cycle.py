@@ -1,4 +1,8 @@
-"""Event trace of CTA 0 of the persistent cycle kernel (GSS_TRACE=1).
+"""(Historical: written for the kernel before the control-warp restructure;
+several events it reads are no longer emitted. The current per-phase
+profile is GSS_DEBUG=256 / 1024 with tools/prof_sweep.py.)
+
+Event trace of CTA 0 of the persistent cycle kernel (GSS_TRACE=1).
 
     python tools/trace_cycle.py --n 10000000 --p 64
 Ring events (arg = stream position q): 20 producer issue, 23 producer passed the
