@@ -20,10 +20,17 @@
 //                   boxes, plus the tile's slice of three CSC index lists
 //                   (pending-update column, scan column, next column) as 1D
 //                   bulk copies.  It runs ahead across slot boundaries.
-//   consumer warps: one warp per tile: patch the pending update into the
-//                   staged tile and commit it, 8 passes of (thread-serial 8
-//                   rows -> warp scan), transform at tied-block ends, and the
-//                   next slot's per-tile record (lane sums needed by the carry).
+//   consumer warps: 16, in tile groups (4 warps for Cox, 8 for Fine-Gray),
+//                   a group per tile: patch the pending update into the staged
+//                   tile and commit it, thread-serial 8-row aggregates -> warp
+//                   scans -> group exchange, transform at tied-block ends, and
+//                   the next slot's per-tile record (in shared memory).
+//   control warp  : owns every cross-slot value (in shared memory); folds the
+//                   records into the in-range carry scan as tiles retire, then
+//                   publishes the CTA payload, joins the grid barrier, gathers
+//                   all payload rows with one bulk copy, runs the replicated
+//                   Engine::finish + coordinate_step and hands the consumers
+//                   the next slot (or a rare all-warp task) at a named barrier.
 // Carry.  A tile's risk-set carry is the sum of all earlier rows.  It is
 // assembled from per-tile records written by the previous slot's consumers;
 // the exp(delta) change of the pending indicator update enters linearly
