@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--c3-p", type=int, default=5000,
                     help="columns of the secondary C3 (Fine-Gray) measurement; 0 = skip")
     ap.add_argument("--c3-cycles", type=int, default=2)
+    ap.add_argument("--no-parity", action="store_true", help="skip the C2 oracle spot-check")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 time-to-fit pair")
     return ap.parse_args()
 
 
@@ -278,6 +280,96 @@ def roofline(n, col_ptr, cycles_ms, accepted_per_cycle, p, launches_per_cycle):
             "kernel": "cycle_kernel<false> (p coordinate slots + 1 objective slot per launch)"}
 
 
+def parity_spot_check(sim, eng, cols=(0, 1777, 4999)):
+    """CHECKER (outside every timed region): the device engine's derivatives
+    and log-likelihood at the fitted beta of the timed C2 cycles against the C
+    oracle (oracle/oracle.c, pinned to the reference's goldens) on the same
+    host data.  Reported as max relative errors; tolerance 1e-10 (north star)."""
+    from oracle import oracle as orc
+    n, p = sim.n, sim.p
+    beta = eng.beta()
+    ds = orc.Sorted(sim.times, np.ascontiguousarray(sim.status, np.int32),
+                    np.arange(n, dtype=np.int64), np.ascontiguousarray(sim.col_ptr),
+                    np.ascontiguousarray(sim.row_idx), np.ones(1), np.ones(p, np.uint8))
+    t0 = time.perf_counter()
+    ref = orc.OracleEngine(ds, "cox")
+    ref.load_beta(beta)
+    ll_d, ll_r = eng.log_likelihood(), ref.log_likelihood()
+    eg, eh = 0.0, 0.0
+    cols = [c for c in cols if c < p]
+    for j in cols:
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        den = max(1.0, abs(a["gradient"]), abs(b["gradient"]), abs(b["fixed_term"]),
+                  abs(b["grad_sum"]))
+        eg = max(eg, abs(a["gradient"] - b["gradient"]) / den)
+        eh = max(eh, abs(a["hessian"] - b["hessian"]) / max(1.0, abs(a["hessian"]),
+                                                            abs(b["hessian"])))
+    ell = abs(ll_d - ll_r) / max(1.0, abs(ll_d), abs(ll_r))
+    worst = max(eg, eh, ell)
+    return {"checker": "C oracle (oracle/oracle.c) on the same host data, at the beta after "
+                       "the timed cycles", "columns": cols,
+            "max_rel_err_gradient": eg, "max_rel_err_hessian": eh, "rel_err_loglik": ell,
+            "tolerance": 1e-10, "pass": bool(worst < 1e-10),
+            "nonzero_beta": int(np.count_nonzero(beta)),
+            "checker_seconds": round(time.perf_counter() - t0, 2)}
+
+
+def run_c1(dist):
+    """Config C1 (BASELINE configs[0]) on the reference's own data
+    (tests/golden/c1_ref.npz, produced by the reference's simulate_cox seed 1):
+    time-to-fit (L1 gamma=sqrt(2), tol 1e-6) end to end through the C ABI from
+    host buffers, beside the reference CPU fit on this box's host cores."""
+    from paper_2204_08183_b200 import capi
+    from tests.golden.make_c1 import load as load_c1
+    c1 = load_c1()
+    gamma = float(c1["gamma"])
+    args = (c1["times"], c1["status"], c1["col_ptr"], c1["row_idx"])
+    # warm the context / first-launch costs once, then time
+    capi.Engine(capi.Dataset(*args, device=dist.local), "cox").fit(
+        penalty="l1", strength=gamma, max_cycles=1)
+    walls, dev_s = [], []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        d = capi.Dataset(*args, device=dist.local)
+        r = capi.Engine(d, "cox").fit(penalty="l1", strength=gamma, tol=1e-6, max_cycles=1000)
+        walls.append(time.perf_counter() - t0)
+        dev_s.append(r["device_seconds"])
+    beta_err = float(np.max(np.abs(r["beta"] - c1["fit_beta"]) /
+                            np.maximum(1.0, np.abs(c1["fit_beta"]))))
+    out = {"workload": "C1: simulate_cox(n=1e5, p=1000, density=0.01, seed=1) from the "
+                       "reference binary; L1 gamma=sqrt(2), tol 1e-6",
+           "gpu_time_to_fit_s": round(float(np.median(walls)), 4),
+           "gpu_device_seconds": round(float(np.median(dev_s)), 4),
+           "cycles": int(r["cycles"]), "nonzero": int(r["nonzero_count"]),
+           "objective": r["objective"], "reference_objective": float(c1["fit_objective"]),
+           "max_rel_err_beta_vs_reference": beta_err,
+           "path": "gss_dataset_pack + gss_engine_create + gss_engine_fit from host arrays"}
+    try:
+        ref = reference_module()
+        threads = len(os.sched_getaffinity(0))
+        n = len(c1["times"])
+        rows = c1["row_ids"][c1["row_idx"]]
+        cols = np.repeat(np.arange(len(c1["col_ptr"]) - 1), np.diff(c1["col_ptr"]))
+        rds = ref.dataset_from_coo(c1["times"][np.argsort(c1["row_ids"])],
+                                   c1["status"][np.argsort(c1["row_ids"])], rows, cols,
+                                   np.ones(len(rows)), len(c1["col_ptr"]) - 1)
+        rw = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            rr = ref.fit(rds, model="cox", penalty="l1", strength=gamma, tol=1e-6,
+                         max_cycles=1000, threads=threads, chunk_size=max(4096, -(-n // threads)))
+            rw.append(time.perf_counter() - t0)
+        out["reference_time_to_fit_s"] = round(float(min(rw)), 4)
+        out["reference_cores"] = threads
+        out["reference_cycles"] = int(rr["cycles"])
+        out["speedup_time_to_fit"] = round(out["reference_time_to_fit_s"] /
+                                           out["gpu_time_to_fit_s"], 2)
+    except Exception as exc:  # pragma: no cover - reference module missing on the box
+        out["reference_time_to_fit_s"] = None
+        out["reference_unavailable"] = str(exc)[:200]
+    return out
+
+
 def run_gss(args, dist):
     from paper_2204_08183_b200 import capi
     dev = dist.local
@@ -302,6 +394,9 @@ def run_gss(args, dist):
     coords = dist.sum(float(K * args.p))
     value = coords / (t_max * 1e-3)
     roof = roofline(args.n, sim.col_ptr, ms[W:W + K], acc_per[W:W + K], args.p, args.p + 1)
+    parity = None
+    if dist.rank == 0 and not args.no_parity:
+        parity = parity_spot_check(sim, eng)
     del eng
     # ---------------- end-to-end through the C ABI from host buffers -----
     e2e_vals, ttf, e2e_cycles = [], [], []
@@ -321,6 +416,7 @@ def run_gss(args, dist):
         e2e_cycles.append(r2["cycles"])
         del e2, d2
     c3 = run_c3(args, dist) if args.c3_p > 0 else None
+    c1 = run_c1(dist) if (dist.rank == 0 and not args.no_c1) else None
     out = {
         "metric": "cox_ccd_coordinate_updates_per_s",
         "value": round(value, 2),
@@ -355,8 +451,13 @@ def run_gss(args, dist):
         "clocks": clocks,
         "fit_objective_after_timed_cycles": res["objective"],
     }
+    if parity is not None:
+        out["parity_c2"] = parity
+    out["secondary"] = {}
     if c3 is not None:
-        out["secondary"] = {"c3_finegray": c3}
+        out["secondary"]["c3_finegray"] = c3
+    if c1 is not None:
+        out["secondary"]["c1_time_to_fit"] = c1
     return out
 
 

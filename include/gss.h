@@ -102,6 +102,17 @@ int64_t gss_dataset_device_bytes(const gss_dataset* ds);
 int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
                       const uint8_t* row_mask, gss_engine** out);
 void gss_engine_destroy(gss_engine* e);
+/*
+ * CTAs of the engine's persistent launches (one per SM by default = the
+ * device's co-resident capacity; 0 restores it).  The tile ranges are
+ * re-partitioned.  Used by the parity tests to put many tiles on each CTA
+ * (the geometry of the full-size fits on small inputs) and by batched
+ * multi-fit launches.  The environment variable GSS_MAX_GRID caps it at
+ * creation.  No reference counterpart (ChunkPlan, scan.hpp:22-46, is the
+ * CPU analogue: it only changes the summation order).
+ */
+int gss_engine_set_grid(gss_engine* e, int grid);
+int gss_engine_grid(gss_engine* e);
 
 /* Engine::load_beta (engine.hpp:46; src/engine.cpp:120-154). */
 int gss_engine_load_beta(gss_engine* e, const double* beta, int64_t p);

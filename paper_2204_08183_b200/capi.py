@@ -31,6 +31,7 @@ EXPORTS = [
     "gss_engine_max_abs_gradient", "gss_engine_last_timing", "gss_engine_grad_hessian_all",
     "gss_engine_cycle_stats", "gss_shard_aggregate", "gss_shard_sums",
     "gss_engine_update_validate", "gss_engine_grad_hessian_separated",
+    "gss_engine_set_grid", "gss_engine_grid",
 ]
 
 
@@ -195,6 +196,15 @@ class Engine:
         if getattr(self, "h", None) and _lib is not None:
             _lib.gss_engine_destroy(self.h)
             self.h = None
+
+    def set_grid(self, grid):
+        """CTAs per launch (0 = one per SM); re-partitions the tile ranges."""
+        check(lib().gss_engine_set_grid(self.h, int(grid)))
+        return self
+
+    @property
+    def grid(self):
+        return lib().gss_engine_grid(self.h)
 
     def load_beta(self, beta):
         b = np.ascontiguousarray(beta, np.float64)

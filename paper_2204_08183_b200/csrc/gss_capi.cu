@@ -136,6 +136,7 @@ struct gss_engine {
   bool weighted = false;
   cudaStream_t stream = nullptr;
   int grid = 1;
+  int max_grid = 1;               // co-resident capacity (payload buffers are sized for it)
   std::vector<uint32_t> h_code;   // device positions
   std::vector<double> h_u, h_g;   // sorted order (accessor)
   std::vector<double> h_beta;
@@ -350,6 +351,60 @@ double penalty_value(const gss_penalty_spec* pen, const std::vector<double>& bet
       acc += beta[j] * beta[j] / (2.0 * pen->strength);
   }
   return acc;
+}
+
+// Static contiguous CTA tile ranges, balanced by estimated tile cost: a tile
+// costs its streaming (1) plus its transform passes (8-row x 32-lane passes
+// holding a tied-block end).  Sets E->grid / prm.grid / prm.cta_tile0.
+int partition_ctas(gss_engine* E, int grid) {
+  const int nt = E->ds->ntiles;
+  grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
+  std::vector<double> w(static_cast<size_t>(nt), 1.0);
+  static const double kPassW =
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
+  for (int t = 0; t < nt; ++t) {
+    int work = 0;
+    for (int pass = 0; pass < kTileRows / 256; ++pass) {
+      bool any = false;
+      for (int r = 0; r < 256 && !any; ++r)
+        any = (E->h_code[size_t(t) * kTileRows + pass * 256 + r] & kCodeCount) != 0;
+      work += any ? 1 : 0;
+    }
+    w[t] = 1.0 + kPassW * work;
+  }
+  double tot = 0.0;
+  for (double x : w) tot += x;
+  std::vector<int32_t> t0(static_cast<size_t>(grid) + 1, 0);
+  double acc = 0.0;
+  int c = 1;
+  for (int t = 0; t < nt && c < grid; ++t) {
+    acc += w[t];
+    // cut after tile t once CTA c-1 holds its share (every CTA keeps >= 1 tile)
+    while (c < grid && acc >= tot * c / grid && t + 1 <= nt - (grid - c)) {
+      t0[c] = t + 1;
+      ++c;
+    }
+  }
+  for (; c < grid; ++c) t0[c] = std::max(t0[c - 1] + 1, nt - (grid - c));
+  t0[grid] = nt;
+  for (int k = 1; k <= grid; ++k)
+    if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
+  if (std::getenv("GSS_VERBOSE")) {
+    for (int k = 0; k < grid; ++k) {
+      double wk = 0.0;
+      for (int t = t0[k]; t < t0[k + 1]; ++t) wk += w[t];
+      std::fprintf(stderr, "cta %d tiles [%d,%d) n=%d cost %.2f\n", k, t0[k], t0[k + 1],
+                   t0[k + 1] - t0[k], wk);
+    }
+  }
+  GSS_CUDA(cudaMemcpy(E->cta_tile0, t0.data(), (grid + 1) * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+  E->grid = grid;
+  E->prm.grid = grid;
+  E->prm.cta_tile0 = E->cta_tile0;
+  // per-tile records / carries of the previous partition are stale
+  E->h_ctl->rec_valid = 0;
+  return GSS_OK;
 }
 
 }  // namespace
@@ -585,7 +640,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   } while (0)
   int maxg = cycle_max_grid(ds->device, E->weighted);
   if (maxg < 1) return bail(fail(GSS_ERR_CUDA, "cycle kernel cannot be resident on this device"));
-  E->grid = std::max(1, std::min(nt, maxg));
+  E->grid = std::max(1, std::min(nt, maxg));  // payload buffers sized for the largest grid
   EK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
   EK(cudaEventCreate(&E->ev0));
   EK(cudaEventCreate(&E->ev1));
@@ -678,48 +733,15 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.recompute_interval = recompute_interval;
   P.grid = E->grid;
   {
-    // cost-balanced contiguous tile ranges: a tile costs its streaming (1)
-    // plus transform passes (8-row x 32-lane passes holding a tied-block end)
-    std::vector<double> w(static_cast<size_t>(nt), 1.0);
-    for (int t = 0; t < nt; ++t) {
-      int work = 0;
-      for (int pass = 0; pass < kTileRows / 256; ++pass) {
-        bool any = false;
-        for (int r = 0; r < 256 && !any; ++r)
-          any = (E->h_code[size_t(t) * kTileRows + pass * 256 + r] & kCodeCount) != 0;
-        work += any ? 1 : 0;
-      }
-      static const double kPassW = std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
-      w[t] = 1.0 + kPassW * work;
+    int mg = maxg;
+    if (const char* cap = std::getenv("GSS_MAX_GRID")) {
+      const int c = std::atoi(cap);
+      if (c > 0) mg = std::min(mg, c);
     }
-    double tot = 0.0;
-    for (double x : w) tot += x;
-    std::vector<int32_t> t0(static_cast<size_t>(E->grid) + 1, 0);
-    double acc = 0.0;
-    int c = 1;
-    for (int t = 0; t < nt && c < E->grid; ++t) {
-      acc += w[t];
-      // cut after tile t once CTA c-1 holds its share (every CTA keeps >= 1 tile)
-      while (c < E->grid && acc >= tot * c / E->grid && t + 1 <= nt - (E->grid - c)) {
-        t0[c] = t + 1;
-        ++c;
-      }
-    }
-    for (; c < E->grid; ++c) t0[c] = std::max(t0[c - 1] + 1, nt - (E->grid - c));
-    t0[E->grid] = nt;
-    for (int k = 1; k <= E->grid; ++k)
-      if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
-    if (std::getenv("GSS_VERBOSE")) {
-      for (int k = 0; k < E->grid; ++k) {
-        double wk = 0.0;
-        for (int t = t0[k]; t < t0[k + 1]; ++t) wk += w[t];
-        std::fprintf(stderr, "cta %d tiles [%d,%d) n=%d cost %.2f\n", k, t0[k], t0[k + 1],
-                     t0[k + 1] - t0[k], wk);
-      }
-    }
-    EK(dalloc(&E->cta_tile0, E->grid + 1));
-    EK(cudaMemcpy(E->cta_tile0, t0.data(), (E->grid + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
-    P.cta_tile0 = E->cta_tile0;
+    EK(dalloc(&E->cta_tile0, maxg + 1));
+    E->max_grid = maxg;
+    int rc2 = partition_ctas(E, std::max(1, std::min(nt, mg)));
+    if (rc2) return bail(rc2);
   }
   P.trec = E->trec;
   P.tcar = E->tcar;
@@ -740,6 +762,19 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
 }
 
 void gss_engine_destroy(gss_engine* e) { delete e; }
+
+int gss_engine_set_grid(gss_engine* E, int grid) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (grid < 0) return fail(GSS_ERR_DOMAIN, "grid must be >= 0");
+  rc = sync_ctl(E);
+  if (rc) return rc;
+  rc = partition_ctas(E, grid == 0 ? E->max_grid : grid);
+  if (rc) return rc;
+  return push_ctl(E);
+}
+
+int gss_engine_grid(gss_engine* E) { return E ? E->grid : 0; }
 
 int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
   int rc = check_engine(E);

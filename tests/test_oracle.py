@@ -127,3 +127,17 @@ def test_finegray_without_competing_is_cox_bitwise():
     for j in range(ds.p):
         assert a.grad_hessian(j) == b.grad_hessian(j)
     assert a.log_likelihood() == b.log_likelihood()
+
+
+def test_oracle_on_reference_c1_data():
+    """The C oracle on config C1's reference-generated data (tests/golden/
+    c1_ref.npz, make_c1.py) reproduces the reference's 3-cycle fit."""
+    from tests.golden.make_c1 import load as load_c1
+    c1 = load_c1()
+    ds = orc.Sorted(c1["times"], c1["status"], np.asarray(c1["row_ids"], np.int64),
+                    c1["col_ptr"], c1["row_idx"], np.ones(len(c1["row_idx"])),
+                    np.ones(len(c1["col_ptr"]) - 1, np.uint8))
+    r = orc.OracleEngine(ds, "cox").fit(penalty="l1", strength=float(c1["gamma"]), max_cycles=3)
+    assert r["cycles"] == 3
+    assert np.max(rel(r["beta"], c1["fit3_beta"])) < 1e-8
+    assert rel(r["objective"], float(c1["fit3_objective"])) < 1e-10
