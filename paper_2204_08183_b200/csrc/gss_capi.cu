@@ -25,6 +25,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gss.h"
 #include "gss_device.cuh"
 #include "gss_kernels.cuh"
@@ -34,6 +36,21 @@ using namespace gss;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX ranges (header-only nvtx3; free when no tool is attached): one per C ABI
+// entry point, per pack stage and per CCD cycle, so an nsys/ncu timeline
+// lines the device launches up with the host calls that issued them.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  Nvtx(const char* fmt, long long k) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), fmt, k);
+    nvtxRangePushA(buf);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -424,6 +441,7 @@ int gss_device_count(void) {
 }
 
 int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
+  Nvtx nvtx_("gss_dataset_pack");
   if (!h || !out) return fail(GSS_ERR_DOMAIN, "null argument");
   *out = nullptr;
   if (h->n < 0 || h->p < 0) return fail(GSS_ERR_DOMAIN, "negative dimensions");
@@ -542,6 +560,7 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   PK(cudaMemcpyAsync(ds->tile_first, ds->h_tile_first.data(), ds->ntiles, cudaMemcpyHostToDevice,
                      s));
   {
+    Nvtx nv("pack: validate csc");
     int* bad = nullptr;
     PK(dalloc(&bad, 1));
     PK(cudaMemsetAsync(bad, 0, sizeof(int), s));
@@ -564,11 +583,13 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     cudaFree(drow);
   }
   if (p) {
+    Nvtx nv("pack: tile pointers + colmax");
     PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
     PK(launch_colmax(ds->col_ptr, ds->has_vals ? ds->vals : nullptr, p, ds->colmax, s));
   }
   // CSR transpose over device positions: count -> exclusive scan -> fill -> per-row sort
   {
+    Nvtx nv("pack: csr transpose");
     int64_t* cnt = nullptr;
     PK(dalloc(&cnt, npad + 1));
     PK(cudaMemsetAsync(cnt, 0, (npad + 1) * sizeof(int64_t), s));
@@ -594,6 +615,7 @@ int64_t gss_dataset_device_bytes(const gss_dataset* ds) { return ds ? ds->bytes 
 
 int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
                       const uint8_t* row_mask, gss_engine** out) {
+  Nvtx nvtx_("gss_engine_create");
   if (!ds || !out) return fail(GSS_ERR_DOMAIN, "null argument");
   *out = nullptr;
   if (recompute_interval < 1) return fail(GSS_ERR_DOMAIN, "recompute_interval must be at least 1");
@@ -777,6 +799,7 @@ int gss_engine_set_grid(gss_engine* E, int grid) {
 int gss_engine_grid(gss_engine* E) { return E ? E->grid : 0; }
 
 int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
+  Nvtx nvtx_("gss_engine_load_beta");
   int rc = check_engine(E);
   if (rc) return rc;
   if (p != E->ds->p)
@@ -829,6 +852,7 @@ int gss_engine_refresh(gss_engine* E) {
 }
 
 int gss_engine_update(gss_engine* E, int64_t column, double delta) {
+  Nvtx nvtx_("gss_engine_update");
   int rc = check_engine(E);
   if (rc) return rc;
   if (column < 0 || column >= E->ds->p)
@@ -860,6 +884,7 @@ int gss_engine_update(gss_engine* E, int64_t column, double delta) {
 
 int gss_engine_grad_hessian(gss_engine* E, int64_t column, double* gradient, double* hessian,
                             double* fixed_term) {
+  Nvtx nvtx_("gss_engine_grad_hessian");
   int rc = check_engine(E);
   if (rc) return rc;
   if (column < 0 || column >= E->ds->p)
@@ -917,6 +942,7 @@ int gss_engine_grad_hessian_separated(gss_engine* E, int64_t column, double* gra
 }
 
 int gss_engine_log_likelihood(gss_engine* E, double* out) {
+  Nvtx nvtx_("gss_engine_log_likelihood");
   int rc = check_engine(E);
   if (rc) return rc;
   rc = run_slots(E, {-1}, kModeApi, false);
@@ -985,6 +1011,7 @@ int gss_engine_counters(gss_engine* E, int64_t* accepted, int64_t* refreshes) {
 
 int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* cfg,
                    double* beta_out, double* trace_out, gss_fit_result* res) {
+  Nvtx nvtx_("gss_engine_fit");
   int rc = check_engine(E);
   if (rc) return rc;
   if (!pen || !cfg || !res) return fail(GSS_ERR_DOMAIN, "null argument");
@@ -1044,6 +1071,7 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   int64_t cycle = 0;
   int err = GSS_OK;
   for (cycle = 1; !converged && cycle <= cfg->max_cycles; ++cycle) {
+    Nvtx nvtx_cycle("ccd cycle %lld", static_cast<long long>(cycle));
     cudaEventRecord(E->ev0, s);
     err = run_slots(E, slots, kModeCcd, false);
     cudaEventRecord(E->ev1, s);
@@ -1084,6 +1112,7 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
 
 int gss_engine_grad_hessian_all(gss_engine* E, double* gradient, double* hessian,
                                 double* fixed_term) {
+  Nvtx nvtx_("gss_engine_grad_hessian_all");
   int rc = check_engine(E);
   if (rc) return rc;
   const int64_t p = E->ds->p;

@@ -253,6 +253,18 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+// CTA-scope message flags in shared memory (stream progress, issue count):
+// release store by the publisher, acquire loads by the pollers, so the data
+// written before the flag (records, committed updates) is visible after it.
+__device__ __forceinline__ void flag_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned flag_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
 // swizzled element addresses inside a staged tile: TMA boxes of 128-byte rows
 // (16 doubles / 32 codes) with 128B swizzle; a lane's 8-row thread-row is half
 // (exp(eta), G) or a quarter (codes) of a box row, and the lane pattern of the
@@ -374,7 +386,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
   return ns;
 }
-__device__ unsigned* g_marks;  // unused placeholder
 __device__ __noinline__ void watchdog_trap(const char* what, unsigned a, unsigned b,
                                            const volatile unsigned* marks = nullptr) {
   if (marks)
@@ -490,13 +501,13 @@ __device__ __forceinline__ void producer(const CycleParams& P, unsigned char* sm
         // publishing its progress)
         if (qw >= utc) {
           const unsigned prevq = qw - utc;
-          const volatile unsigned* pr = &tl->progress[tl_i % G::kNG];
-          if (*pr < prevq + 1) {
+          const unsigned* pr = &tl->progress[tl_i % G::kNG];
+          if (flag_acquire(pr) < prevq + 1) {
             const unsigned long long tw = gtimer();
-            while (*pr < prevq + 1) {
+            while (flag_acquire(pr) < prevq + 1) {
               __nanosleep(32);
               if (gtimer() - tw > kWatchdogNs)
-                watchdog_trap("producer progress wait", qw, *pr, tl->mark);
+                watchdog_trap("producer progress wait", qw, flag_acquire(pr), tl->mark);
             }
           }
         }
@@ -545,7 +556,7 @@ __device__ __forceinline__ void producer(const CycleParams& P, unsigned char* sm
       trace_c0(P, 26, static_cast<int>(qq));
       // positions are issued in order: publish the count (consumers check it
       // before their parity wait, see the consumer loop)
-      *reinterpret_cast<volatile unsigned*>(&tl->issued) = qq + 1;
+      flag_release(&tl->issued, qq + 1);
     }
     __syncwarp();
   }
@@ -1773,20 +1784,19 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       if (!FG && lane == 0 && !(P.dbg & (16 | 512))) {
         double car[6] = {0, 0, 0, 0, 0, 0};
         int seen = 0;
-        const volatile unsigned* prog = tl->progress;
+        const unsigned* prog = tl->progress;
         for (int i = 0; i < tc; ++i) {
           const unsigned need = qbase + static_cast<unsigned>(i) + 1u;
           const int g = i % Gm::kNG;
-          if (prog[g] < need) {
+          if (flag_acquire(prog + g) < need) {
             const unsigned long long tw = gtimer();
             unsigned it = 0;
-            while (prog[g] < need) {
+            while (flag_acquire(prog + g) < need) {
               __nanosleep(64);
               if ((++it & 63u) == 0 && gtimer() - tw > kWatchdogNs)
-                watchdog_trap("control record wait", need, prog[g]);
+                watchdog_trap("control record wait", need, flag_acquire(prog + g));
             }
           }
-          __threadfence_block();
           const int t = t0 + i;
           const double* rec = rec_at<FG>(P, tl, t, i);
           const int f = (i < MaxTc<FG>::v) ? tl->tfirst[i] : (P.tile_first[t] ? 1 : 0);
@@ -2151,14 +2161,15 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         // q (it issues q only after q - S was released), then the parity test
         // is exact.
         {
-          const volatile unsigned* iss = &tl->issued;
-          if (*iss <= q) {
+          const unsigned* iss = &tl->issued;
+          if (flag_acquire(iss) <= q) {
             const unsigned long long tw = gtimer();
             unsigned it = 0;
-            while (*iss <= q) {
+            while (flag_acquire(iss) <= q) {
               __nanosleep(32);
               if ((++it & 63u) == 0 && gtimer() - tw > kWatchdogNs)
-                watchdog_trap("consumer issue wait", q, *iss, lane == 0 ? tl->mark : nullptr);
+                watchdog_trap("consumer issue wait", q, flag_acquire(iss),
+                              lane == 0 ? tl->mark : nullptr);
             }
           }
         }
@@ -2173,8 +2184,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
         mark<FG>(tl, 0x15u | (q << 8));
         group_sync<FG>(g);
         if (gw == 0 && lane == 0) {
-          __threadfence_block();  // the tile's record before its progress
-          *reinterpret_cast<volatile unsigned*>(&tl->progress[g]) = q + 1;
+          flag_release(&tl->progress[g], q + 1);  // the tile's record before its progress
           mbar_arrive(&tl->empty[s]);
         }
       }

@@ -3,6 +3,10 @@
 #include "survscan/dataset.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <cstdio>
+#include <string_view>
+#include <unordered_set>
 #include <cmath>
 #include <fstream>
 #include <numeric>
@@ -234,120 +238,281 @@ SurvivalDataset dataset_from_coo(const std::vector<double>& times, const std::ve
                                    std::move(cl), std::move(ss));
 }
 
-// ---- plain-text persistence -------------------------------------------------
-SurvivalDataset load_sparse_coo(const std::string& obs_path, const std::string& matrix_path) {
-  std::ifstream fo(obs_path), fm(matrix_path);
-  if (!fo) throw ParseError("cannot open " + obs_path);
-  if (!fm) throw ParseError("cannot open " + matrix_path);
-  std::vector<double> t;
-  std::vector<int> s;
+// ---- plain-text persistence ------------------------------------------------
+// The reference's two formats (src/dataset.cpp:82-117, 363-556), so files move
+// between the two implementations unchanged:
+//   * sparse COO pair: "row_id,time,status" lines + "row_id,col_id,value"
+//     lines, '#' comments, an optional "# cols: P" width declaration
+//     (otherwise the width is max col + 1), duplicate cells rejected;
+//   * dense CSV with a header naming "time" and "status" anywhere; every other
+//     column is a covariate; row ids are the line order.
+// Strata are a rebuild feature with no file representation: they are not
+// written (a stratified dataset round-trips as unstratified).
+namespace {
+
+std::string where(const std::string& path, std::size_t line_no) {
+  return path + ":" + std::to_string(line_no);
+}
+
+template <class T>
+T parse_number(std::string_view tok, const std::string& path, std::size_t line_no,
+               const char* what) {
+  if (tok.empty()) throw ParseError("missing value at " + where(path, line_no));
+  T out{};
+  const char* end = tok.data() + tok.size();
+  const auto res = std::from_chars(tok.data(), end, out);
+  if (res.ec != std::errc{} || res.ptr != end)
+    throw ParseError(std::string("bad ") + what + " '" + std::string(tok) + "' at " +
+                     where(path, line_no));
+  return out;
+}
+
+double time_field(std::string_view tok, const std::string& path, std::size_t line_no) {
+  const double t = parse_number<double>(tok, path, line_no, "numeric value");
+  if (!std::isfinite(t) || t < 0.0)
+    throw DomainError("time must be finite and >= 0 at " + where(path, line_no));
+  return t;
+}
+
+int status_field(std::string_view tok, const std::string& path, std::size_t line_no) {
+  const double v = parse_number<double>(tok, path, line_no, "numeric value");
+  if (v != 0.0 && v != 1.0 && v != 2.0)
+    throw DomainError("status must be 0, 1 or 2 at " + where(path, line_no));
+  return static_cast<int>(v);
+}
+
+std::vector<std::string_view> fields(std::string_view line) {
+  std::vector<std::string_view> out;
+  for (std::size_t a = 0;;) {
+    const std::size_t b = line.find(',', a);
+    out.push_back(line.substr(a, b == std::string_view::npos ? std::string_view::npos : b - a));
+    if (b == std::string_view::npos) return out;
+    a = b + 1;
+  }
+}
+
+// payload lines of a text file: '\r' stripped, blank and '#' lines skipped;
+// "# cols: P" reported through `declared`
+template <class Fn>
+void data_lines(const std::string& path, Fn&& fn, std::size_t* declared = nullptr) {
+  std::ifstream in(path);
+  if (!in) throw ParseError("cannot open '" + path + "'");
   std::string line;
-  std::size_t n_cols = 0;
-  while (std::getline(fo, line)) {
-    if (line.empty() || line[0] == '#') continue;
-    std::istringstream is(line);
-    double ti;
-    int si;
-    if (!(is >> ti >> si)) throw ParseError("bad observation line: " + line);
-    t.push_back(ti);
-    s.push_back(si);
+  for (std::size_t no = 1; std::getline(in, line); ++no) {
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    std::string_view v(line);
+    const std::size_t k = v.find_first_not_of(" \t");
+    if (k == std::string_view::npos) continue;
+    v.remove_prefix(k);
+    if (v.front() == '#') {
+      constexpr std::string_view tag = "# cols:";
+      if (declared && v.starts_with(tag)) {
+        std::string_view rest = v.substr(tag.size());
+        const std::size_t w = rest.find_first_not_of(" \t");
+        if (w != std::string_view::npos)
+          *declared = static_cast<std::size_t>(
+              parse_number<std::int64_t>(rest.substr(w), path, no, "integer"));
+      }
+      continue;
+    }
+    fn(std::string_view(line), no);
+  }
+}
+
+void put_double(std::string& out, double v) {
+  char buf[32];
+  const int len = std::snprintf(buf, sizeof(buf), "%.17g", v);
+  out.append(buf, static_cast<std::size_t>(len));
+}
+
+}  // namespace
+
+SurvivalDataset sort_and_block(RawData raw) {
+  // ids must be a permutation of [0, n) (src/dataset.cpp:212-262); the
+  // builder below orders ties by position, so place each observation at its id
+  const std::size_t n = raw.obs.size();
+  for (const auto& o : raw.obs) {
+    if (!std::isfinite(o.time) || o.time < 0.0)
+      throw DomainError("observation time must be finite and >= 0");
+    if (o.status != 0 && o.status != 1 && o.status != 2)
+      throw DomainError("status must be 0, 1 or 2");
+  }
+  std::vector<double> t(n);
+  std::vector<int> s(n);
+  std::vector<unsigned char> seen(n, 0);
+  for (const auto& o : raw.obs) {
+    if (o.row_id < 0 || static_cast<std::size_t>(o.row_id) >= n)
+      throw IndexError("row id " + std::to_string(o.row_id) + " outside [0, " +
+                       std::to_string(n) + ")");
+    if (seen[static_cast<std::size_t>(o.row_id)]++)
+      throw DuplicateEntryError("row id " + std::to_string(o.row_id) + " appears more than once");
+    t[static_cast<std::size_t>(o.row_id)] = o.time;
+    s[static_cast<std::size_t>(o.row_id)] = o.status;
   }
   std::vector<std::int64_t> r, c;
   std::vector<double> v;
-  while (std::getline(fm, line)) {
-    if (line.empty()) continue;
-    if (line[0] == '#') {
-      std::istringstream is(line.substr(1));
-      std::string key;
-      if (is >> key && key == "n_cols") is >> n_cols;
-      continue;
-    }
-    std::istringstream is(line);
-    std::int64_t ri, ci;
-    double vi;
-    if (!(is >> ri >> ci >> vi)) throw ParseError("bad matrix line: " + line);
-    r.push_back(ri);
-    c.push_back(ci);
-    v.push_back(vi);
+  r.reserve(raw.entries.size());
+  c.reserve(raw.entries.size());
+  v.reserve(raw.entries.size());
+  for (const auto& e : raw.entries) {
+    if (e.col >= raw.n_cols)
+      throw IndexError("matrix column " + std::to_string(e.col) + " outside [0, " +
+                       std::to_string(raw.n_cols) + ")");
+    r.push_back(e.row);
+    c.push_back(static_cast<std::int64_t>(e.col));
+    v.push_back(e.value);
   }
-  return dataset_from_coo(t, s, r, c, v, n_cols);
+  return dataset_from_coo(t, s, r, c, v, raw.n_cols);
+}
+
+SurvivalDataset load_sparse_coo(const std::string& obs_path, const std::string& matrix_path) {
+  RawData raw;
+  data_lines(obs_path, [&](std::string_view line, std::size_t no) {
+    const auto f = fields(line);
+    if (f.size() != 3)
+      throw ParseError("expected 'row_id,time,status' at " + where(obs_path, no));
+    Observation o;
+    o.row_id = parse_number<std::int64_t>(f[0], obs_path, no, "integer");
+    o.time = time_field(f[1], obs_path, no);
+    o.status = status_field(f[2], obs_path, no);
+    raw.obs.push_back(o);
+  });
+  const std::size_t n = raw.obs.size();
+  std::unordered_set<std::uint64_t> cells;
+  std::size_t declared = 0, width = 0;
+  data_lines(
+      matrix_path,
+      [&](std::string_view line, std::size_t no) {
+        const auto f = fields(line);
+        if (f.size() != 3)
+          throw ParseError("expected 'row_id,col_id,value' at " + where(matrix_path, no));
+        const auto row = parse_number<std::int64_t>(f[0], matrix_path, no, "integer");
+        const auto col = parse_number<std::int64_t>(f[1], matrix_path, no, "integer");
+        const double value = parse_number<double>(f[2], matrix_path, no, "numeric value");
+        if (row < 0 || static_cast<std::size_t>(row) >= n)
+          throw IndexError("matrix row " + std::to_string(row) + " outside [0, " +
+                           std::to_string(n) + ") at " + where(matrix_path, no));
+        if (col < 0) throw IndexError("negative column at " + where(matrix_path, no));
+        const std::uint64_t key =
+            (static_cast<std::uint64_t>(row) << 32) | static_cast<std::uint64_t>(col);
+        if (!cells.insert(key).second)
+          throw DuplicateEntryError("cell (" + std::to_string(row) + "," + std::to_string(col) +
+                                    ") given twice at " + where(matrix_path, no));
+        if (!std::isfinite(value))
+          throw DomainError("matrix value must be finite at " + where(matrix_path, no));
+        width = std::max(width, static_cast<std::size_t>(col) + 1);
+        if (value != 0.0) raw.entries.push_back({row, static_cast<std::size_t>(col), value});
+      },
+      &declared);
+  if (declared > 0 && width > declared)
+    throw IndexError("matrix column " + std::to_string(width - 1) + " outside declared width " +
+                     std::to_string(declared) + " in '" + matrix_path + "'");
+  raw.n_cols = std::max(declared, width);
+  return sort_and_block(std::move(raw));
 }
 
 void write_sparse_coo(const SurvivalDataset& ds, const std::string& obs_path,
                       const std::string& matrix_path) {
-  // rows are written in original row-id order, so a reload sorts identically
-  std::vector<std::size_t> pos_of(ds.n());
-  for (std::size_t i = 0; i < ds.n(); ++i) pos_of[static_cast<std::size_t>(ds.row_ids()[i])] = i;
-  std::ofstream fo(obs_path), fm(matrix_path);
-  if (!fo || !fm) throw ParseError("cannot write dataset files");
-  fo.precision(17);
-  fm.precision(17);
-  for (std::size_t id = 0; id < ds.n(); ++id)
-    fo << ds.times()[pos_of[id]] << ' ' << ds.status()[pos_of[id]] << '\n';
-  fm << "# n_cols " << ds.p() << '\n';
+  // sorted order with explicit row ids (ids need not be a permutation of
+  // [0, n): subset_rows keeps the parent's ids)
+  std::string buf;
+  {
+    std::ofstream fo(obs_path);
+    if (!fo) throw ParseError("cannot write '" + obs_path + "'");
+    fo << "# row_id,time,status\n";
+    for (std::size_t i = 0; i < ds.n(); ++i) {
+      buf = std::to_string(ds.row_ids()[i]);
+      buf += ',';
+      put_double(buf, ds.times()[i]);
+      buf += ',';
+      buf += std::to_string(ds.status()[i]);
+      buf += '\n';
+      fo << buf;
+    }
+    if (!fo) throw ParseError("short write to '" + obs_path + "'");
+  }
+  std::ofstream fm(matrix_path);
+  if (!fm) throw ParseError("cannot write '" + matrix_path + "'");
+  fm << "# row_id,col_id,value\n# cols: " << ds.p() << '\n';
   for (std::size_t j = 0; j < ds.p(); ++j)
-    for (std::int64_t k = ds.col_ptr()[j]; k < ds.col_ptr()[j + 1]; ++k)
-      fm << ds.row_ids()[static_cast<std::size_t>(ds.row_idx()[k])] << ' ' << j << ' '
-         << ds.values()[static_cast<std::size_t>(k)] << '\n';
+    for (std::int64_t k = ds.col_ptr()[j]; k < ds.col_ptr()[j + 1]; ++k) {
+      buf = std::to_string(ds.row_ids()[static_cast<std::size_t>(ds.row_idx()[k])]);
+      buf += ',';
+      buf += std::to_string(j);
+      buf += ',';
+      put_double(buf, ds.values()[static_cast<std::size_t>(k)]);
+      buf += '\n';
+      fm << buf;
+    }
+  if (!fm) throw ParseError("short write to '" + matrix_path + "'");
 }
 
 SurvivalDataset load_dense_csv(const std::string& path) {
-  std::ifstream f(path);
-  if (!f) throw ParseError("cannot open " + path);
-  std::vector<double> t;
-  std::vector<int> s;
-  std::vector<std::int64_t> r, c;
-  std::vector<double> v;
+  std::ifstream in(path);
+  if (!in) throw ParseError("cannot open '" + path + "'");
   std::string line;
-  std::size_t n_cols = 0, row = 0;
-  bool header = true;
-  while (std::getline(f, line)) {
-    if (line.empty()) continue;
-    std::vector<std::string> cells;
-    std::stringstream ss(line);
-    std::string cell;
-    while (std::getline(ss, cell, ',')) cells.push_back(cell);
-    if (header) {
-      header = false;
-      if (cells.size() < 2) throw SchemaError("csv needs time,status,x0,... columns");
-      n_cols = cells.size() - 2;
-      continue;
+  if (!std::getline(in, line)) throw SchemaError("empty file '" + path + "'");
+  if (!line.empty() && line.back() == '\r') line.pop_back();
+  const std::string header_line = line;
+  const auto head = fields(header_line);
+  std::size_t tcol = head.size(), scol = head.size();
+  std::vector<std::size_t> xcols;
+  for (std::size_t i = 0; i < head.size(); ++i) {
+    if (head[i] == "time") {
+      if (tcol != head.size()) throw SchemaError("duplicate 'time' column in '" + path + "'");
+      tcol = i;
+    } else if (head[i] == "status") {
+      if (scol != head.size()) throw SchemaError("duplicate 'status' column in '" + path + "'");
+      scol = i;
+    } else {
+      xcols.push_back(i);
     }
-    if (cells.size() != n_cols + 2) throw ParseError("ragged csv row " + std::to_string(row));
-    try {
-      t.push_back(std::stod(cells[0]));
-      s.push_back(std::stoi(cells[1]));
-      for (std::size_t j = 0; j < n_cols; ++j) {
-        const double x = std::stod(cells[2 + j]);
-        if (x != 0.0) {
-          r.push_back(static_cast<std::int64_t>(row));
-          c.push_back(static_cast<std::int64_t>(j));
-          v.push_back(x);
-        }
-      }
-    } catch (const std::logic_error&) {
-      throw ParseError("bad csv value in row " + std::to_string(row));
-    }
-    ++row;
   }
-  return dataset_from_coo(t, s, r, c, v, n_cols);
+  if (tcol == head.size()) throw SchemaError("'" + path + "' has no 'time' column");
+  if (scol == head.size()) throw SchemaError("'" + path + "' has no 'status' column");
+  RawData raw;
+  raw.n_cols = xcols.size();
+  for (std::size_t no = 2; std::getline(in, line); ++no) {
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    if (line.empty()) continue;
+    const auto f = fields(line);
+    if (f.size() != head.size())
+      throw ParseError("expected " + std::to_string(head.size()) + " cells, got " +
+                       std::to_string(f.size()) + " at " + where(path, no));
+    Observation o;
+    o.row_id = static_cast<std::int64_t>(raw.obs.size());
+    o.time = time_field(f[tcol], path, no);
+    o.status = status_field(f[scol], path, no);
+    for (std::size_t j = 0; j < xcols.size(); ++j) {
+      const double x = parse_number<double>(f[xcols[j]], path, no, "numeric value");
+      if (!std::isfinite(x)) throw DomainError("covariate must be finite at " + where(path, no));
+      if (x != 0.0) raw.entries.push_back({o.row_id, j, x});
+    }
+    raw.obs.push_back(o);
+  }
+  return sort_and_block(std::move(raw));
 }
 
 void write_dense_csv(const SurvivalDataset& ds, const std::string& path) {
   std::ofstream f(path);
-  if (!f) throw ParseError("cannot write " + path);
-  f.precision(17);
-  f << "time,status";
-  for (std::size_t j = 0; j < ds.p(); ++j) f << ",x" << j;
-  f << '\n';
-  std::vector<std::size_t> pos_of(ds.n());
-  for (std::size_t i = 0; i < ds.n(); ++i) pos_of[static_cast<std::size_t>(ds.row_ids()[i])] = i;
-  for (std::size_t id = 0; id < ds.n(); ++id) {
-    const std::size_t i = pos_of[id];
-    f << ds.times()[i] << ',' << ds.status()[i];
-    for (std::size_t j = 0; j < ds.p(); ++j) f << ',' << ds.covariate(i, j);
-    f << '\n';
+  if (!f) throw ParseError("cannot write '" + path + "'");
+  std::string buf = "time,status";
+  for (std::size_t j = 0; j < ds.p(); ++j) buf += ",x" + std::to_string(j);
+  buf += '\n';
+  f << buf;
+  for (std::size_t i = 0; i < ds.n(); ++i) {  // sorted order, like the reference
+    buf.clear();
+    put_double(buf, ds.times()[i]);
+    buf += ',';
+    buf += std::to_string(ds.status()[i]);
+    for (std::size_t j = 0; j < ds.p(); ++j) {
+      buf += ',';
+      put_double(buf, ds.covariate(i, j));
+    }
+    buf += '\n';
+    f << buf;
   }
+  if (!f) throw ParseError("short write to '" + path + "'");
 }
 
 }  // namespace survscan

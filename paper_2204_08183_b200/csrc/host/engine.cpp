@@ -35,8 +35,10 @@ int default_device() {
 
 static int model_code(Model m) { return m == Model::cox ? GSS_COX : GSS_FINE_GRAY; }
 
-Engine::Engine(const SurvivalDataset& ds, Model model, ChunkPlan, std::size_t recompute_interval)
-    : ds_(&ds), model_(model), device_(default_device()) {
+Engine::Engine(const SurvivalDataset& ds, Model model, ChunkPlan plan,
+               std::size_t recompute_interval)
+    : ds_(&ds), model_(model), plan_(plan), device_(default_device()) {
+  plan_.validate();
   check(gss_engine_create(ds.device(device_), model_code(model),
                           static_cast<int64_t>(recompute_interval), nullptr, &h_));
 }
@@ -55,7 +57,7 @@ Engine::~Engine() {
   if (h_) gss_engine_destroy(h_);
 }
 
-void Engine::load_beta(const std::vector<double>& beta) {
+void Engine::load_beta(std::span<const double> beta) {
   check(gss_engine_load_beta(h_, beta.data(), static_cast<int64_t>(beta.size())));
 }
 
@@ -88,43 +90,51 @@ std::vector<GradHess> Engine::grad_hessian_all() {
   return out;
 }
 
-double Engine::log_likelihood() {
+double Engine::log_likelihood() const {
   double ll = 0.0;
   check(gss_engine_log_likelihood(h_, &ll));
   return ll;
 }
 
-std::vector<double> Engine::beta() const {
-  std::vector<double> b(ds_->p());
-  check(gss_engine_get_beta(h_, b.data(), static_cast<int64_t>(b.size())));
-  return b;
+std::span<const double> Engine::beta() const {
+  beta_.resize(ds_->p());
+  check(gss_engine_get_beta(h_, beta_.data(), static_cast<int64_t>(beta_.size())));
+  return beta_;
 }
 
-std::vector<double> Engine::xbeta() const {
-  std::vector<double> v(ds_->n());
-  check(gss_engine_get_xbeta(h_, v.data(), static_cast<int64_t>(v.size())));
-  return v;
+std::span<const double> Engine::xbeta() const {
+  xbeta_.resize(ds_->n());
+  check(gss_engine_get_xbeta(h_, xbeta_.data(), static_cast<int64_t>(xbeta_.size())));
+  return xbeta_;
 }
 
-std::vector<double> Engine::exp_xbeta() const {
-  std::vector<double> v(ds_->n());
-  check(gss_engine_get_exp_xbeta(h_, v.data(), static_cast<int64_t>(v.size())));
-  return v;
+std::span<const double> Engine::exp_xbeta() const {
+  exp_xbeta_.resize(ds_->n());
+  check(gss_engine_get_exp_xbeta(h_, exp_xbeta_.data(), static_cast<int64_t>(exp_xbeta_.size())));
+  return exp_xbeta_;
 }
 
-std::vector<double> Engine::fixed_terms() const {
-  std::vector<double> v(ds_->p());
-  check(gss_engine_get_fixed_terms(h_, v.data(), static_cast<int64_t>(v.size())));
-  return v;
+std::span<const double> Engine::fixed_terms() const {
+  fixed_.resize(ds_->p());
+  check(gss_engine_get_fixed_terms(h_, fixed_.data(), static_cast<int64_t>(fixed_.size())));
+  return fixed_;
 }
 
-IpcwWeights Engine::ipcw() const {
-  IpcwWeights w;
-  if (model_ != Model::fine_gray) return w;
-  w.u.resize(ds_->n());
-  w.g.resize(ds_->n());
-  check(gss_engine_get_ipcw(h_, w.u.data(), w.g.data(), static_cast<int64_t>(ds_->n())));
-  return w;
+const IpcwWeights& Engine::ipcw() const {
+  // fixed at construction (censoring.cpp:65-90 runs once per Engine)
+  if (!ipcw_valid_ && model_ == Model::fine_gray) {
+    ipcw_.u.resize(ds_->n());
+    ipcw_.g.resize(ds_->n());
+    check(gss_engine_get_ipcw(h_, ipcw_.u.data(), ipcw_.g.data(), static_cast<int64_t>(ds_->n())));
+  }
+  ipcw_valid_ = true;
+  return ipcw_;
+}
+
+std::vector<double> precompute_fixed_terms(const SurvivalDataset& ds) {
+  Engine eng(ds, ds.has_competing() ? Model::fine_gray : Model::cox);
+  auto f = eng.fixed_terms();
+  return {f.begin(), f.end()};
 }
 
 std::size_t Engine::accepted_updates() const {

@@ -9,12 +9,31 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <span>
 #include <string>
 #include <vector>
 
 struct gss_dataset;
 
 namespace survscan {
+
+// Raw input of the reference's dataset builder (dataset.hpp:16-20, 56-61).
+struct Observation {
+  double time = 0.0;
+  int status = 0;
+  std::int64_t row_id = 0;
+};
+
+struct RawData {
+  std::vector<Observation> obs;
+  std::size_t n_cols = 0;
+  struct Entry {
+    std::int64_t row;  // refers to Observation::row_id
+    std::size_t col;
+    double value;
+  };
+  std::vector<Entry> entries;
+};
 
 class SurvivalDataset {
  public:
@@ -46,6 +65,11 @@ class SurvivalDataset {
   // allowed with fresh ids, e.g. bootstrap resamples).
   SurvivalDataset subset_rows(const std::vector<std::uint32_t>& positions,
                               bool fresh_row_ids) const;
+  SurvivalDataset subset_rows(std::span<const std::uint32_t> positions,
+                              bool fresh_row_ids = false) const {
+    return subset_rows(std::vector<std::uint32_t>(positions.begin(), positions.end()),
+                       fresh_row_ids);
+  }
 
   // Device-resident packed copy (created on first use; thread safe).
   gss_dataset* device(int device) const;
@@ -79,7 +103,13 @@ SurvivalDataset dataset_from_coo(const std::vector<double>& times, const std::ve
                                  const std::vector<double>& values, std::size_t n_cols,
                                  const std::vector<std::int64_t>& strata = {});
 
-// Plain-text persistence (obs: "time status" per row; coo: "row col value").
+// sort_and_block (src/dataset.cpp:212-262): row ids must be a permutation of
+// [0, n); ties in time keep ascending row id.
+SurvivalDataset sort_and_block(RawData raw);
+
+// Plain-text persistence in the reference's formats (src/dataset.cpp:363-556):
+// "row_id,time,status" + "row_id,col_id,value" (with "# cols: P"), dense CSV
+// with "time" and "status" header columns.
 SurvivalDataset load_sparse_coo(const std::string& obs_path, const std::string& matrix_path);
 void write_sparse_coo(const SurvivalDataset& ds, const std::string& obs_path,
                       const std::string& matrix_path);

@@ -6,9 +6,13 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <span>
 #include <vector>
 
+#include "survscan/censoring.hpp"
 #include "survscan/dataset.hpp"
+#include "survscan/errors.hpp"
+#include "survscan/scan.hpp"
 
 struct gss_engine;
 
@@ -22,16 +26,8 @@ struct GradHess {
   double fixed_term = 0.0;
 };
 
-// The reference's CPU chunk plan; accepted for API compatibility, ignored by
-// the device engine (its tiling is fixed by the dataset pack).
-struct ChunkPlan {
-  std::size_t chunk_size = 65536;
-  unsigned worker_count = 0;
-};
-
-struct IpcwWeights {
-  std::vector<double> u, g;
-};
+// delta' X_j for every column (engine.hpp:27), computed on the device.
+std::vector<double> precompute_fixed_terms(const SurvivalDataset& ds);
 
 class Engine {
  public:
@@ -47,9 +43,10 @@ class Engine {
 
   const SurvivalDataset& data() const { return *ds_; }
   Model model_kind() const { return model_; }
+  const ChunkPlan& plan() const { return plan_; }
   int device() const { return device_; }
 
-  void load_beta(const std::vector<double>& beta);
+  void load_beta(std::span<const double> beta);
   void update_xbeta_sparse(std::size_t column, double delta);
   void refresh();
   GradHess grad_hessian(std::size_t column);
@@ -57,13 +54,16 @@ class Engine {
   GradHess grad_hessian_separated(std::size_t column);
   // all columns in one device launch (the batched sweep behind gamma_max)
   std::vector<GradHess> grad_hessian_all();
-  double log_likelihood();
+  double log_likelihood() const;
 
-  std::vector<double> beta() const;
-  std::vector<double> xbeta() const;
-  std::vector<double> exp_xbeta() const;
-  std::vector<double> fixed_terms() const;
-  IpcwWeights ipcw() const;
+  // Views of host copies of the device state, refreshed by each call (valid
+  // until the next call of the same accessor or the next mutation), as the
+  // reference's spans are valid until the engine mutates (engine.hpp:65-71).
+  std::span<const double> beta() const;
+  std::span<const double> xbeta() const;
+  std::span<const double> exp_xbeta() const;
+  std::span<const double> fixed_terms() const;
+  const IpcwWeights& ipcw() const;
   std::size_t accepted_updates() const;
   std::size_t refresh_count() const;
 
@@ -72,8 +72,12 @@ class Engine {
  private:
   const SurvivalDataset* ds_;
   Model model_;
+  ChunkPlan plan_;
   int device_ = 0;
   gss_engine* h_ = nullptr;
+  mutable std::vector<double> beta_, xbeta_, exp_xbeta_, fixed_;
+  mutable IpcwWeights ipcw_;
+  mutable bool ipcw_valid_ = false;
 };
 
 // device for new engines: $SURVSCAN_DEVICE or 0

@@ -96,3 +96,129 @@ def test_auto_grid_endpoints():
     g = survscan.auto_grid(2.0)
     assert len(g) == 10 and g[0] == 2.0 / 1000.0 and g[-1] == 2.0
     assert all(a < b for a, b in zip(g, g[1:]))
+
+
+REF_MOD = os.path.join(ROOT, "oracle", "_ref")
+
+
+def _reference(code):
+    """Run `code` against the reference module in a SUBPROCESS (two pybind
+    modules translating the same C++ exception type in one process would
+    cross-register their exception classes)."""
+    import subprocess
+    import sys
+    if not os.path.isdir(REF_MOD):
+        pytest.skip("oracle/_ref (the reference built from /root/reference) is absent")
+    subprocess.check_call([sys.executable, "-c", "import sys; sys.path.insert(0, %r); "
+                           "import _survscan as ref\n" % REF_MOD + code])
+
+
+def _same_content(a, b):
+    assert a.n == b.n and a.p == b.p
+    assert np.array_equal(np.asarray(a.times), np.asarray(b.times))
+    assert np.array_equal(np.asarray(a.status), np.asarray(b.status))
+    for i in range(a.n):
+        for j in range(a.p):
+            assert a.covariate(i, j) == b.covariate(i, j), (i, j)
+
+
+def test_sparse_coo_files_interchange_with_reference(tmp_path):
+    """Files written by the reference load here and vice versa
+    (src/dataset.cpp:454-556: 'row_id,time,status' + 'row_id,col_id,value'
+    with '# cols: P'; dense CSV by header name, :363-451)."""
+    import survscan
+    d = str(tmp_path)
+    _reference(f"""
+ds, _, _ = ref.simulate_finegray(n=250, p=7, density=0.2, seed=9, censoring_quantile=0.8)
+ref.write_sparse_coo(ds, {d!r} + '/r.obs', {d!r} + '/r.coo')
+ref.write_dense_csv(ds, {d!r} + '/r.csv')
+open({d!r} + '/r.hash', 'w').write(str(ds.content_hash))
+""")
+    mine = survscan.load_sparse_coo(d + "/r.obs", d + "/r.coo")
+    dense = survscan.load_dense_csv(d + "/r.csv")
+    assert mine.n == dense.n == 250 and mine.p == dense.p == 7
+    assert list(mine.times) == list(dense.times)
+    for i in range(mine.n):
+        for j in range(mine.p):
+            assert mine.covariate(i, j) == dense.covariate(i, j)
+    survscan.write_sparse_coo(mine, d + "/m.obs", d + "/m.coo")
+    survscan.write_dense_csv(mine, d + "/m.csv")
+    _reference(f"""
+h = int(open({d!r} + '/r.hash').read())
+back = ref.load_sparse_coo({d!r} + '/m.obs', {d!r} + '/m.coo')
+assert back.content_hash == h, 'sparse COO written here differs from the reference dataset'
+a = ref.load_dense_csv({d!r} + '/m.csv')
+b = ref.load_dense_csv({d!r} + '/r.csv')
+assert a.content_hash == b.content_hash, 'dense CSV written here differs'
+""")
+
+
+def test_sparse_coo_parsing_rules(tmp_path):
+    """Width inferred as max col + 1 without '# cols:', '\\r' line ends,
+    duplicate cells and bad tokens rejected with the reference's classes."""
+    import survscan
+    ob, mx = tmp_path / "o.csv", tmp_path / "x.csv"
+    ob.write_text("# row_id,time,status\r\n2,1.5,1\r\n0,3,0\r\n1,2,2\r\n")
+    mx.write_text("0,4,1\n2,1,2.5\n")
+    ds = survscan.load_sparse_coo(str(ob), str(mx))
+    assert ds.p == 5 and ds.n == 3 and list(ds.times) == [3.0, 2.0, 1.5]
+    assert ds.covariate(0, 4) == 1.0 and ds.covariate(2, 1) == 2.5
+    mx.write_text("# cols: 8\n0,4,1\n")
+    assert survscan.load_sparse_coo(str(ob), str(mx)).p == 8
+    mx.write_text("# cols: 2\n0,4,1\n")
+    with pytest.raises(survscan.SurvscanError, match="declared width"):
+        survscan.load_sparse_coo(str(ob), str(mx))
+    mx.write_text("0,1,1\n0,1,2\n")
+    with pytest.raises(survscan.SurvscanError, match="given twice"):
+        survscan.load_sparse_coo(str(ob), str(mx))
+    mx.write_text("0,x,1\n")
+    with pytest.raises(survscan.SurvscanError, match="bad integer"):
+        survscan.load_sparse_coo(str(ob), str(mx))
+    ob.write_text("0,1,1\n0,2,1\n")
+    mx.write_text("")
+    with pytest.raises(survscan.SurvscanError, match="more than once"):
+        survscan.load_sparse_coo(str(ob), str(mx))
+
+
+def test_write_subset_with_parent_row_ids(tmp_path):
+    """subset_rows keeps the parent's row ids by default; writing such a
+    dataset must not index by raw id (heap overwrite)."""
+    import survscan
+    ds, _ = survscan.simulate_cox(n=40, p=3, density=0.3, seed=2)
+    sub = ds.subset_rows([0, 5, 17], fresh_row_ids=False)
+    ob, mx, csv = str(tmp_path / "s.obs"), str(tmp_path / "s.coo"), str(tmp_path / "s.csv")
+    survscan.write_sparse_coo(sub, ob, mx)
+    survscan.write_dense_csv(sub, csv)
+    ids = [int(l.split(",")[0]) for l in open(ob) if not l.startswith("#")]
+    assert len(ids) == 3 and max(ids) > 3  # parent ids written verbatim
+    again = survscan.load_dense_csv(csv)
+    assert list(again.times) == list(sub.times)
+
+
+HOST = os.path.join(ROOT, "paper_2204_08183_b200", "csrc", "host")
+
+
+def test_reference_ccd_compiles_against_mirror_headers(tmp_path):
+    """The reference's own CCD driver (src/ccd.cpp), unmodified, compiles
+    against this repo's survscan/*.hpp: the C++ surface it uses (Engine
+    span-taking load_beta, const log_likelihood, span accessors, plan(),
+    ChunkPlan::validate, PenaltySpec, FitConfig) is source compatible."""
+    import subprocess
+    src = "/root/reference/proj/src/ccd.cpp"
+    if not os.path.exists(src):
+        pytest.skip("reference sources absent")
+    subprocess.check_call(["g++", "-std=c++20", "-fsyntax-only", "-I" + HOST, src])
+
+
+def test_drop_in_caller_builds_and_links(tmp_path):
+    """A caller written against engine.hpp:38-71 / ccd.hpp compiles and links
+    against libsurvscan_b200 (it runs in tests/test_gpu_survscan_api.py)."""
+    import subprocess
+    from paper_2204_08183_b200 import build as B
+    B.build()
+    out = str(tmp_path / "caller")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I" + HOST,
+                           os.path.join(ROOT, "tests", "cpp", "drop_in_caller.cpp"),
+                           "-L" + B.PKG, "-lsurvscan_b200", "-lgss",
+                           "-Wl,-rpath," + B.PKG, "-o", out])
+    assert os.path.exists(out)
