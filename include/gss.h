@@ -175,6 +175,26 @@ int gss_engine_fit(gss_engine* e, const gss_penalty_spec* pen, const gss_fit_con
                    double* beta_out, double* trace_out, gss_fit_result* out);
 
 /*
+ * Batched multi-fit ("a single larger
+ * kernel to perform many repetitions of k-fold cross-validation"): fits
+ * count engines (e.g. the folds x lambda tasks of cross_validate,
+ * src/crossval.cpp:153-174, or bootstrap resamples, :218-257), each exactly as
+ * gss_engine_fit would (same results), but up to max_active of them (<= 24;
+ * <= 0 = 24) advance together: every launch of the cycle kernel runs one CCD
+ * cycle of every active fit, each on its own share of the SMs with its own
+ * grid barrier, so small-N fits stop paying a whole GPU's exchange latency per
+ * coordinate.  A fit that converges (or fails) leaves the batch and the next
+ * queued one joins.  All engines must live on one device and share p.
+ * pens[count]; cfg shared; beta_out [count][p] (may be NULL); results[count];
+ * status[count] (may be NULL): the gss_status of each fit.  Returns the first
+ * failing fit's status (GSS_OK if all succeeded); device_seconds (may be NULL)
+ * = CUDA-event time of all batched cycle launches.
+ */
+int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_spec* pens,
+                  const gss_fit_config* cfg, int max_active, double* beta_out,
+                  gss_fit_result* results, int32_t* status, double* device_seconds);
+
+/*
  * Engine::grad_hessian for every column at the engine's current beta in ONE
  * device launch (the batched sweep behind gamma_max, src/crossval.cpp:104-110).
  * Each output is [p] (any may be NULL).

@@ -31,7 +31,7 @@ EXPORTS = [
     "gss_engine_max_abs_gradient", "gss_engine_last_timing", "gss_engine_grad_hessian_all",
     "gss_engine_cycle_stats", "gss_shard_aggregate", "gss_shard_sums",
     "gss_engine_update_validate", "gss_engine_grad_hessian_separated",
-    "gss_engine_set_grid", "gss_engine_grid",
+    "gss_engine_set_grid", "gss_engine_grid", "gss_fit_batch",
 ]
 
 
@@ -323,3 +323,38 @@ class Engine:
         L.gss_engine_cycle_stats.restype = ctypes.c_int64
         k = L.gss_engine_cycle_stats(self.h, _p(ms), _p(acc), ctypes.c_int64(max_cycles))
         return ms[:k].copy(), acc[:k].copy()
+
+
+def fit_batch(engines, penalty="l1", strengths=None, tol=1e-6, max_cycles=1000, trust_init=1.0,
+              max_active=0):
+    """gss_fit_batch: fit every engine (one CCD cycle of all active fits per
+    launch).  strengths: one per engine (or a scalar).  Returns (list of fit
+    dicts or GssError per engine, device seconds)."""
+    k = len(engines)
+    if k == 0:
+        return [], 0.0
+    p = engines[0].ds.p
+    kind = {"none": 0, "l1": 1, "l2": 2}[penalty]
+    if strengths is None or np.isscalar(strengths):
+        strengths = [0.0 if strengths is None else float(strengths)] * k
+    pens = (PenaltySpec * k)(*[PenaltySpec(kind, float(g), None) for g in strengths])
+    cfg = FitConfig(tol, max_cycles, trust_init)
+    hs = (ctypes.c_void_p * k)(*[e.h.value for e in engines])
+    beta = np.zeros((k, p))
+    res = (FitResult * k)()
+    st = np.zeros(k, np.int32)
+    dev_s = ctypes.c_double()
+    lib().gss_fit_batch(hs, ctypes.c_int64(k), pens, ctypes.byref(cfg), int(max_active),
+                        _p(beta), res, _p(st), ctypes.byref(dev_s))
+    out = []
+    for i in range(k):
+        if st[i]:
+            out.append(GssError(int(st[i]), "batched fit %d failed" % i))
+            continue
+        r = res[i]
+        out.append({"beta": beta[i].copy(), "objective": r.objective, "cycles": r.cycles,
+                    "converged": bool(r.converged), "nonzero_count": r.nonzero_count,
+                    "skipped_steps": r.skipped_steps,
+                    "monotonicity_violations": r.monotonicity_violations,
+                    "wall_seconds": r.wall_seconds, "device_seconds": r.device_seconds})
+    return out, dev_s.value

@@ -157,7 +157,7 @@ struct gss_engine {
   std::vector<uint32_t> h_code;   // device positions
   std::vector<double> h_u, h_g;   // sorted order (accessor)
   std::vector<double> h_beta;
-  std::vector<int32_t> h_slots;
+  std::vector<int32_t> h_slots;   // slots of the staged CCD cycle
   // device
   double *eta = nullptr, *e = nullptr, *scratch = nullptr, *g = nullptr;
   uint32_t* code = nullptr;
@@ -179,6 +179,20 @@ struct gss_engine {
   int64_t last_launches = 0;
   std::vector<double> cycle_ms;
   std::vector<int64_t> cycle_accepted;
+  // state of the fit in progress (fit_begin / fit_after_cycle / fit_end)
+  struct FitState {
+    gss_penalty_spec pen{};
+    std::vector<uint8_t> exempt;
+    gss_fit_config cfg{};
+    std::vector<double> trace;
+    gss_fit_result res{};
+    double prev = 0.0;
+    bool converged = false, done = false;
+    int64_t cycle = 0;
+    int err = GSS_OK;
+    std::chrono::steady_clock::time_point t0;
+    double dev_ms = 0.0;
+  } fs;
 
   ~gss_engine() {
     cudaSetDevice(ds->device);
@@ -1009,13 +1023,20 @@ int gss_engine_counters(gss_engine* E, int64_t* accepted, int64_t* refreshes) {
   return GSS_OK;
 }
 
-int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* cfg,
-                   double* beta_out, double* trace_out, gss_fit_result* res) {
-  Nvtx nvtx_("gss_engine_fit");
+}  // extern "C"
+
+namespace {
+
+// fit_with_engine (src/ccd.cpp:131-184) in three phases, so that one engine
+// (gss_engine_fit) or many (gss_fit_batch: one launch per cycle for all of
+// them) share the same per-fit host logic.
+int fit_begin(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* cfg) {
   int rc = check_engine(E);
   if (rc) return rc;
-  if (!pen || !cfg || !res) return fail(GSS_ERR_DOMAIN, "null argument");
-  const auto t0 = std::chrono::steady_clock::now();
+  if (!pen || !cfg) return fail(GSS_ERR_DOMAIN, "null argument");
+  auto& F = E->fs;
+  F = gss_engine::FitState{};
+  F.t0 = std::chrono::steady_clock::now();
   const int64_t p = E->ds->p;
   // PenaltySpec::validate / FitConfig::validate (src/ccd.cpp:37-69)
   if (pen->kind < 0 || pen->kind > 2) return fail(GSS_ERR_DOMAIN, "unknown penalty");
@@ -1028,6 +1049,13 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   if (cfg->max_cycles < 1) return fail(GSS_ERR_DOMAIN, "max_cycles must be >= 1");
   if (!std::isfinite(cfg->trust_init) || cfg->trust_init <= 0.0)
     return fail(GSS_ERR_DOMAIN, "trust_init must be > 0");
+  F.pen = *pen;
+  if (pen->exempt) {
+    F.exempt.assign(pen->exempt, pen->exempt + p);
+    F.pen.exempt = F.exempt.data();
+  }
+  F.cfg = *cfg;
+  F.trace.assign(static_cast<size_t>(cfg->max_cycles) + 1, 0.0);
   std::vector<double> zero(static_cast<size_t>(p), 0.0);
   rc = gss_engine_load_beta(E, zero.data(), p);  // ccd.cpp:137
   if (rc) return rc;
@@ -1052,61 +1080,222 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   E->h_ctl->err_col = -1;
   rc = push_ctl(E);
   if (rc) return rc;
-
-  *res = gss_fit_result{};
   double ll = 0.0;
   rc = gss_engine_log_likelihood(E, &ll);
   if (rc) return rc;
-  double prev = ll - penalty_value(pen, E->h_beta);
-  if (trace_out) trace_out[0] = prev;
-  bool converged = p == 0;
-
-  // one cycle = p coordinate slots + the objective slot, one kernel launch
+  F.prev = ll - penalty_value(&F.pen, E->h_beta);
+  F.trace[0] = F.prev;
+  F.converged = p == 0;
+  F.done = F.converged;
+  E->cycle_ms.clear();
+  E->cycle_accepted.clear();
+  // one cycle = p coordinate slots + the objective slot
   std::vector<int32_t> slots(static_cast<size_t>(p + 1));
   for (int64_t j = 0; j < p; ++j) slots[j] = static_cast<int32_t>(j);
   slots[p] = -1;
-  double dev_ms = 0.0;
-  E->cycle_ms.clear();
-  E->cycle_accepted.clear();
-  int64_t cycle = 0;
-  int err = GSS_OK;
-  for (cycle = 1; !converged && cycle <= cfg->max_cycles; ++cycle) {
-    Nvtx nvtx_cycle("ccd cycle %lld", static_cast<long long>(cycle));
+  E->h_slots = slots;
+  GSS_CUDA(cudaMemcpyAsync(E->slot_col, slots.data(), slots.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice, s));
+  GSS_CUDA(cudaStreamSynchronize(s));
+  return GSS_OK;
+}
+
+// parameters of one CCD-cycle launch of E (slots staged by fit_begin)
+CycleParams cycle_params(const gss_engine* E) {
+  CycleParams P = E->prm;
+  P.slot_col = E->slot_col;
+  P.nslots = static_cast<int>(E->h_slots.size());
+  P.mode = kModeCcd;
+  P.slot_out = nullptr;
+  P.ext = nullptr;
+  P.shard_out = nullptr;
+  P.prologue_only = 0;
+  P.reuse_records = 0;
+  return P;
+}
+
+// after a cycle launch of E completed (stream synchronised by the caller)
+int fit_after_cycle(gss_engine* E, double ms) {
+  auto& F = E->fs;
+  const int64_t p = E->ds->p;
+  int rc = sync_ctl(E);
+  if (rc) return F.err = rc;
+  ++F.cycle;
+  F.dev_ms += ms;
+  E->cycle_ms.push_back(ms);
+  E->cycle_accepted.push_back(E->h_ctl->accepted);
+  if (p) GSS_CUDA(cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost));
+  if (E->h_ctl->err_code) {
+    F.err = device_error(E, "fit");
+    F.done = true;
+    return F.err;
+  }
+  F.res.cycles = F.cycle;
+  const double obj = E->h_ctl->loglik - penalty_value(&F.pen, E->h_beta);
+  F.trace[F.cycle] = obj;
+  if (obj < F.prev - 1e-10) ++F.res.monotonicity_violations;
+  if (std::abs(obj - F.prev) / std::max(1.0, std::abs(obj)) < F.cfg.tolerance) F.converged = true;
+  F.prev = obj;
+  if (F.converged || F.cycle >= F.cfg.max_cycles) F.done = true;
+  return GSS_OK;
+}
+
+int fit_end(gss_engine* E, double* beta_out, double* trace_out, gss_fit_result* res) {
+  auto& F = E->fs;
+  E->last_ms = F.dev_ms;
+  E->last_launches = F.res.cycles;
+  if (F.err) return F.err;
+  F.res.converged = F.converged ? 1 : 0;
+  F.res.objective = F.prev;
+  F.res.skipped_steps = E->h_ctl->skipped;
+  F.res.nonzero_count = 0;
+  const int64_t p = E->ds->p;
+  for (int64_t j = 0; j < p; ++j) F.res.nonzero_count += E->h_beta[j] != 0.0;
+  if (beta_out) std::copy(E->h_beta.begin(), E->h_beta.end(), beta_out);
+  if (trace_out) std::copy(F.trace.begin(), F.trace.begin() + F.cycle + 1, trace_out);
+  F.res.device_seconds = F.dev_ms * 1e-3;
+  F.res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - F.t0).count();
+  *res = F.res;
+  return GSS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* cfg,
+                   double* beta_out, double* trace_out, gss_fit_result* res) {
+  Nvtx nvtx_("gss_engine_fit");
+  if (!res) return fail(GSS_ERR_DOMAIN, "null argument");
+  *res = gss_fit_result{};
+  int rc = fit_begin(E, pen, cfg);
+  if (rc) return rc;
+  cudaStream_t s = E->stream;
+  while (!E->fs.done) {
+    Nvtx nvtx_cycle("ccd cycle %lld", static_cast<long long>(E->fs.cycle + 1));
+    const CycleParams P = cycle_params(E);
     cudaEventRecord(E->ev0, s);
-    err = run_slots(E, slots, kModeCcd, false);
+    GSS_CUDA(launch_cycle(&E->tm_e, &E->tm_code, &E->tm_g, P, s));
     cudaEventRecord(E->ev1, s);
-    if (err) break;
-    err = sync_ctl(E);
-    if (err) break;
+    GSS_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, E->ev0, E->ev1);
-    dev_ms += ms;
-    E->cycle_ms.push_back(ms);
-    E->cycle_accepted.push_back(E->h_ctl->accepted);
-    if (p) cudaMemcpy(E->h_beta.data(), E->beta, p * sizeof(double), cudaMemcpyDeviceToHost);
-    if (E->h_ctl->err_code) {
-      err = device_error(E, "fit");
-      break;
-    }
-    res->cycles = cycle;
-    const double obj = E->h_ctl->loglik - penalty_value(pen, E->h_beta);
-    if (trace_out) trace_out[cycle] = obj;
-    if (obj < prev - 1e-10) ++res->monotonicity_violations;
-    if (std::abs(obj - prev) / std::max(1.0, std::abs(obj)) < cfg->tolerance) converged = true;
-    prev = obj;
+    if (fit_after_cycle(E, ms)) break;
   }
-  E->last_ms = dev_ms;
-  E->last_launches = res->cycles;
-  if (err) return err;
-  res->converged = converged ? 1 : 0;
-  res->objective = prev;
-  res->skipped_steps = E->h_ctl->skipped;
-  res->nonzero_count = 0;
-  for (int64_t j = 0; j < p; ++j) res->nonzero_count += E->h_beta[j] != 0.0;
-  if (beta_out) std::copy(E->h_beta.begin(), E->h_beta.end(), beta_out);
-  res->device_seconds = dev_ms * 1e-3;
-  res->wall_seconds =
-      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return fit_end(E, beta_out, trace_out, res);
+}
+
+int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_spec* pens,
+                  const gss_fit_config* cfg, int max_active, double* beta_out,
+                  gss_fit_result* results, int32_t* status, double* device_seconds) {
+  Nvtx nvtx_("gss_fit_batch");
+  if (count < 0 || (count > 0 && (!engines || !pens || !cfg || !results)))
+    return fail(GSS_ERR_DOMAIN, "null argument");
+  if (count == 0) return GSS_OK;
+  const int dev = engines[0]->ds->device;
+  for (int64_t i = 0; i < count; ++i) {
+    if (!engines[i]) return fail(GSS_ERR_DOMAIN, "null engine handle");
+    if (engines[i]->ds->device != dev)
+      return fail(GSS_ERR_DOMAIN, "gss_fit_batch: all engines must live on one device");
+    for (int64_t j = 0; j < i; ++j)
+      if (engines[j] == engines[i]) return fail(GSS_ERR_DOMAIN, "gss_fit_batch: repeated engine");
+  }
+  GSS_CUDA(cudaSetDevice(dev));
+  const int64_t p0 = engines[0]->ds->p;
+  std::vector<int> grid0(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) {
+    results[i] = gss_fit_result{};
+    if (status) status[i] = GSS_OK;
+    grid0[i] = engines[i]->grid;
+  }
+  double total_ms = 0.0;
+  // engines of one launch share the kernel instantiation: weighted
+  // (Fine-Gray with competing rows) and unweighted fits go in separate queues
+  int first_err = GSS_OK;
+  std::string first_msg;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool weighted = pass == 1;
+    std::vector<int64_t> queue;
+    for (int64_t i = 0; i < count; ++i)
+      if (engines[i]->weighted == weighted) queue.push_back(i);
+    if (queue.empty()) continue;
+    const int maxg = engines[queue[0]]->max_grid;
+    int slots = max_active > 0 ? max_active : kMaxBatch;
+    slots = std::max(1, std::min({slots, kMaxBatch, maxg, static_cast<int>(queue.size())}));
+    const int share = std::max(1, maxg / slots);
+    size_t next = 0;
+    std::vector<int64_t> active;
+    auto finish = [&](int64_t i, int rc) {
+      gss_engine* E = engines[i];
+      if (rc == GSS_OK)
+        rc = fit_end(E, beta_out ? beta_out + i * p0 : nullptr, nullptr, &results[i]);
+      if (E->grid != grid0[i]) {  // give the engine its own grid back
+        const int rc2 = partition_ctas(E, grid0[i]);
+        if (rc2 == GSS_OK) push_ctl(E);
+      }
+      if (status) status[i] = rc;
+      if (rc && first_err == GSS_OK) {
+        first_err = rc;
+        first_msg = g_last_error;
+      }
+    };
+    auto join = [&]() {
+      while (active.size() < static_cast<size_t>(slots) && next < queue.size()) {
+        const int64_t i = queue[next++];
+        gss_engine* E = engines[i];
+        if (E->ds->p != p0) {
+          finish(i, fail(GSS_ERR_DOMAIN, "gss_fit_batch: engines differ in p"));
+          continue;
+        }
+        int rc = partition_ctas(E, share);
+        if (!rc) rc = push_ctl(E);
+        if (!rc) rc = fit_begin(E, &pens[i], cfg);
+        if (rc || E->fs.done) {
+          finish(i, rc);
+          continue;
+        }
+        active.push_back(i);
+      }
+    };
+    join();
+    cudaStream_t s = engines[queue[0]]->stream;
+    cudaEvent_t e0 = engines[queue[0]]->ev0, e1 = engines[queue[0]]->ev1;
+    std::vector<CycleParams> prm;
+    std::vector<BatchEntry> ent;
+    while (!active.empty()) {
+      Nvtx nvtx_cycle("batched ccd cycle (%lld fits)", static_cast<long long>(active.size()));
+      prm.resize(active.size());
+      ent.resize(active.size());
+      for (size_t a = 0; a < active.size(); ++a) {
+        gss_engine* E = engines[active[a]];
+        prm[a] = cycle_params(E);
+        ent[a] = BatchEntry{&E->tm_e, &E->tm_code, &E->tm_g, &prm[a]};
+      }
+      cudaEventRecord(e0, s);
+      GSS_CUDA(launch_cycle_batch(ent.data(), static_cast<int>(ent.size()), s));
+      cudaEventRecord(e1, s);
+      GSS_CUDA(cudaStreamSynchronize(s));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      total_ms += ms;
+      std::vector<int64_t> still;
+      for (int64_t i : active) {
+        gss_engine* E = engines[i];
+        const int rc = fit_after_cycle(E, ms);
+        if (rc || E->fs.done)
+          finish(i, rc);
+        else
+          still.push_back(i);
+      }
+      active.swap(still);
+      join();
+    }
+  }
+  if (device_seconds) *device_seconds = total_ms * 1e-3;
+  if (first_err) {
+    g_last_error = first_msg;
+    return first_err;
+  }
   return GSS_OK;
 }
 

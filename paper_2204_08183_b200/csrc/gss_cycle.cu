@@ -45,6 +45,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 
 #include "gss_device.cuh"
 #include "gss_kernels.cuh"
@@ -2039,11 +2040,9 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
 // ---------------------------------------------------------------------------
 // the persistent cycle kernel
 // ---------------------------------------------------------------------------
-template <bool FG>
+template <bool FG, int K>
 __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
-    cycle_kernel(const __grid_constant__ CUtensorMap tm_e,
-                 const __grid_constant__ CUtensorMap tm_code,
-                 const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CycleParams P) {
+    cycle_kernel(const __grid_constant__ LaunchParams<K> L) {
   using Gm = Geo<FG>;
   constexpr int W = Gm::kW, S = Gm::kS;
   constexpr int NC = 32 * W;  // consumer threads
@@ -2051,7 +2050,14 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Tail<FG>* tl = reinterpret_cast<Tail<FG>*>(smem + size_t(S) * Gm::kStage);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cta = (P.dbg & 64) ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x);
+  // this CTA's engine (fit) and its CTA index inside that engine's grid
+  int f = 0;
+  if constexpr (K > 1) {
+    while (f + 1 < L.nfit && static_cast<int>(blockIdx.x) >= L.cta_base[f + 1]) ++f;
+  }
+  const CycleParams& P = L.P[f];
+  const int bid = static_cast<int>(blockIdx.x) - (K > 1 ? L.cta_base[f] : 0);
+  const int cta = (P.dbg & 64) ? P.grid - 1 - bid : bid;
   const int G = P.grid;
   // static contiguous tile ranges, balanced by estimated tile cost (host,
   // per engine); P.cta_tile0[c] = first tile of CTA c, [G] = ntiles
@@ -2111,7 +2117,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   }
 
   if (warp > W) {
-    producer<FG>(P, smem, tl, t0, tc, &tm_e, &tm_code, &tm_g, warp - W - 1);
+    producer<FG>(P, smem, tl, t0, tc, &L.tm_e[f], &L.tm_code[f], &L.tm_g[f], warp - W - 1);
     return;
   }
   const bool rec_ok = (P.mode == kModeCcd || P.reuse_records) && ctl->rec_valid &&
@@ -2218,18 +2224,41 @@ size_t cycle_smem_bytes(bool weighted) {
   return weighted ? smem_total<true>() : smem_total<false>();
 }
 
+namespace {
+template <bool FG, int K>
+void set_smem_attr() {
+  cudaFuncSetAttribute(cycle_kernel<FG, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem_total<FG>()));
+}
+
+template <bool FG, int K>
+cudaError_t launch_k(const LaunchParams<K>& L, int grid, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Geo<FG>::kThreads);
+  cfg.dynamicSmemBytes = smem_total<FG>();
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cycle_kernel<FG, K>, L);
+}
+}  // namespace
+
 int cycle_max_grid(int device, bool weighted) {
   int sms = 0, n = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (weighted) {
-    cudaFuncSetAttribute(cycle_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_total<true>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<true>, Geo<true>::kThreads,
+    set_smem_attr<true, 1>();
+    set_smem_attr<true, kMaxBatch>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<true, 1>, Geo<true>::kThreads,
                                                   smem_total<true>());
   } else {
-    cudaFuncSetAttribute(cycle_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_total<false>()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<false>, Geo<false>::kThreads,
+    set_smem_attr<false, 1>();
+    set_smem_attr<false, kMaxBatch>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, cycle_kernel<false, 1>, Geo<false>::kThreads,
                                                   smem_total<false>());
   }
   return n > 0 ? (sms < kMaxGrid ? sms : kMaxGrid) : 0;
@@ -2237,22 +2266,37 @@ int cycle_max_grid(int device, bool weighted) {
 
 cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,
                          const CUtensorMap* tm_g, const CycleParams& prm, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.gridDim = dim3(prm.grid);
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (prm.weighted) {
-    cfg.blockDim = dim3(Geo<true>::kThreads);
-    cfg.dynamicSmemBytes = smem_total<true>();
-    return cudaLaunchKernelEx(&cfg, cycle_kernel<true>, *tm_e, *tm_code, *tm_g, prm);
+  LaunchParams<1> L;
+  L.tm_e[0] = *tm_e;
+  L.tm_code[0] = *tm_code;
+  L.tm_g[0] = *tm_g;
+  L.P[0] = prm;
+  L.nfit = 1;
+  L.cta_base[0] = 0;
+  L.cta_base[1] = prm.grid;
+  return prm.weighted ? launch_k<true, 1>(L, prm.grid, s) : launch_k<false, 1>(L, prm.grid, s);
+}
+
+cudaError_t launch_cycle_batch(const BatchEntry* en, int k, cudaStream_t s) {
+  if (k < 1 || k > kMaxBatch) return cudaErrorInvalidValue;
+  if (k == 1) return launch_cycle(en[0].tm_e, en[0].tm_code, en[0].tm_g, *en[0].prm, s);
+  static LaunchParams<kMaxBatch> L;  // 17 KB: not on the host stack (callers serialise per device)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const bool w = en[0].prm->weighted != 0;
+  int base = 0;
+  for (int i = 0; i < k; ++i) {
+    if ((en[i].prm->weighted != 0) != w) return cudaErrorInvalidValue;
+    L.tm_e[i] = *en[i].tm_e;
+    L.tm_code[i] = *en[i].tm_code;
+    L.tm_g[i] = *en[i].tm_g;
+    L.P[i] = *en[i].prm;
+    L.cta_base[i] = base;
+    base += en[i].prm->grid;
   }
-  cfg.blockDim = dim3(Geo<false>::kThreads);
-  cfg.dynamicSmemBytes = smem_total<false>();
-  return cudaLaunchKernelEx(&cfg, cycle_kernel<false>, *tm_e, *tm_code, *tm_g, prm);
+  L.cta_base[k] = base;
+  L.nfit = k;
+  return w ? launch_k<true, kMaxBatch>(L, base, s) : launch_k<false, kMaxBatch>(L, base, s);
 }
 
 }  // namespace gss

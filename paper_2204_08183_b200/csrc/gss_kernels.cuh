@@ -116,9 +116,32 @@ struct CycleParams {
   int reuse_records;           // API mode: records from a prologue-only launch are valid
 };
 
+// Kernel parameter block of one cycle-kernel launch over K engines (fits):
+// CTAs [cta_base[f], cta_base[f+1]) run engine f with its own parameters,
+// TMA descriptors, grid barrier and payload buffers.  K = 1 is the single-fit
+// launch; K = kMaxBatch the batched multi-fit launch (CV folds x lambda grid,
+// bootstrap resamples).  Lives in the parameter (constant) bank.
+constexpr int kMaxBatch = 24;
+template <int K>
+struct LaunchParams {
+  CUtensorMap tm_e[K], tm_code[K], tm_g[K];
+  CycleParams P[K];
+  int nfit;
+  int cta_base[K + 1];
+};
+struct BatchEntry {
+  const CUtensorMap* tm_e;
+  const CUtensorMap* tm_code;
+  const CUtensorMap* tm_g;
+  const CycleParams* prm;
+};
+
 // launchers (gss_cycle.cu)
 cudaError_t launch_cycle(const CUtensorMap* tm_e, const CUtensorMap* tm_code,
                          const CUtensorMap* tm_g, const CycleParams& prm, cudaStream_t s);
+// one launch for k <= kMaxBatch engines of the same kind (all weighted or
+// none); their grids must fit the device together
+cudaError_t launch_cycle_batch(const BatchEntry* entries, int k, cudaStream_t s);
 int cycle_max_grid(int device, bool weighted);
 size_t cycle_smem_bytes(bool weighted);
 

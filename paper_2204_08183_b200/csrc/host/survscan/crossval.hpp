@@ -45,6 +45,8 @@ double held_out_loglik(const SurvivalDataset& ds, const std::vector<std::uint32_
                        std::uint32_t fold, Model model, const std::vector<double>& beta,
                        const ChunkPlan& plan = {});
 double gamma_max(const SurvivalDataset& ds, Model model, const ChunkPlan& plan = {});
+// the same on a given device (-1 = $SURVSCAN_DEVICE or 0)
+double gamma_max(const SurvivalDataset& ds, Model model, int device);
 std::vector<double> auto_grid(double top);
 // Pieces of cross_validate for multi-process drivers (one process per GPU):
 // the resolved grid, the event-free-fold precheck, the per-task fold scores
@@ -71,14 +73,35 @@ CVResult cross_validate(const SurvivalDataset& ds, Model model, PenaltyKind kind
                         const CVConfig& cv, const FitConfig& fit_config = {},
                         const std::vector<int>& devices = {});
 
+struct BootstrapDraw {
+  double value = 0.0;  // fitted beta[coefficient_index] of the resample
+  bool failed = false;
+};
 struct BootstrapInterval {
   double lower = 0.0;
   double upper = 0.0;
   std::uint32_t failed_resamples = 0;
 };
+// bootstrap_interval (src/crossval.cpp:218-257) with the resamples' fits
+// batched on each device and dealt over devices (and, through the pieces
+// below, over ranks): resample b draws from derive_seed(seed, 0, b) as the
+// reference does, so the draws and the interval equal the reference's.
 BootstrapInterval bootstrap_interval(const SurvivalDataset& ds, Model model,
                                      const PenaltySpec& penalty, const FitConfig& fit_config,
-                                     std::size_t coefficient_index, std::uint32_t resamples,
-                                     std::uint64_t seed);
+                                     std::size_t coefficient_index, std::uint32_t resamples = 200,
+                                     std::uint64_t seed = 0, const std::vector<int>& devices = {});
+
+// the sorted row positions of resample b (derive_seed(seed, 0, b) stream)
+std::vector<std::uint32_t> bootstrap_indices(std::size_t n, std::uint64_t seed,
+                                            std::uint32_t resample);
+// pieces for multi-process drivers: draws of the listed resamples, then the
+// resample-ordered merge (> 10% failures -> DomainError, type-7 quantiles)
+std::vector<BootstrapDraw> bootstrap_run(const SurvivalDataset& ds, Model model,
+                                         const PenaltySpec& penalty, const FitConfig& fit_config,
+                                         std::size_t coefficient_index,
+                                         const std::vector<std::uint32_t>& resample_ids,
+                                         std::uint64_t seed, const std::vector<int>& devices = {});
+BootstrapInterval bootstrap_merge(const std::vector<BootstrapDraw>& draws,
+                                  std::uint32_t resamples);
 
 }  // namespace survscan

@@ -66,9 +66,25 @@ def merge_scores(grid: Sequence[float], repetitions: int,
     return {"curve": curve, "selected": curve[best]["strength"], "failed_replicates": failed}
 
 
+def local_device() -> int:
+    """This process's GPU: LOCAL_RANK (torchrun), else the current CUDA device,
+    else 0 — never the global rank (wrong on multi-node jobs)."""
+    import os
+    if "LOCAL_RANK" in os.environ:
+        return int(os.environ["LOCAL_RANK"])
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return 0
+
+
 def device_task_runner(ds, model: str, penalty: str, grid, folds: int, repetitions: int,
                        seed: int, tol: float, max_cycles: int, device: int) -> TaskRunner:
-    """Tasks on this rank's GPU through the C++ mirror (survscan.cv_run_tasks)."""
+    """Tasks on this rank's GPU through the C++ mirror (survscan.cv_run_tasks:
+    every fold fit of the rank's tasks advances in batched multi-fit launches)."""
     import survscan
 
     def run(tasks):
@@ -78,28 +94,63 @@ def device_task_runner(ds, model: str, penalty: str, grid, folds: int, repetitio
     return run
 
 
+def _gather_checked(dist, world, local, err):
+    """All-gather (payload, error) from every rank; if any rank failed, raise
+    the same error on EVERY rank (no rank is left waiting in a collective)."""
+    parts = [(local, err)]
+    if dist is not None and world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, (local, err))
+    bad = [(r, e) for r, (_, e) in enumerate(parts) if e is not None]
+    if bad:
+        r, e = bad[0]
+        raise RuntimeError(f"rank {r} failed: {e}")
+    return [p for p, _ in parts]
+
+
+def _broadcast(dist, world, obj):
+    if dist is None or world == 1:
+        return obj
+    box = [obj]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
 def cross_validate_distributed(ds, model: str = "cox", penalty: str = "l1",
                                grid: Sequence[float] = (), folds: int = 10,
                                repetitions: int = 10, seed: int = 0, tol: float = 1e-6,
                                max_cycles: int = 1000, device: Optional[int] = None,
                                task_runner: Optional[TaskRunner] = None,
                                final_fit: bool = True) -> dict:
-    """C4 across ranks.  Every rank returns the same merged result."""
+    """C4 across ranks.  Every rank returns the same merged result (or raises
+    the same error)."""
     dist, rank, world = _dist()
     import survscan
-    grid = list(grid) if len(grid) else list(survscan.cv_grid(ds, model))
+    dev = local_device() if device is None else device
+    grid = list(grid)
+    if not grid:  # gamma_max sweep once, on rank 0's GPU, then broadcast
+        res = None
+        if rank == 0:
+            try:
+                res = (list(survscan.cv_grid(ds, model, device=dev)), None)
+            except Exception as exc:  # noqa: BLE001 - re-raised on every rank
+                res = (None, f"{type(exc).__name__}: {exc}")
+        res = _broadcast(dist, world, res)
+        if res[1] is not None:
+            raise RuntimeError(f"rank 0 failed: {res[1]}")
+        grid = res[0]
     survscan.cv_check_folds(ds, folds, repetitions, seed, len(grid))
     n_tasks = len(grid) * repetitions
     mine = shard_tasks(n_tasks, rank, world)
     if task_runner is None:
         task_runner = device_task_runner(ds, model, penalty, grid, folds, repetitions, seed, tol,
-                                         max_cycles, rank if device is None else device)
-    local = list(zip(mine, task_runner(mine)))
-    if dist is not None and world > 1:
-        parts = [None] * world
-        dist.all_gather_object(parts, local)
-    else:
-        parts = [local]
+                                         max_cycles, dev)
+    local, err = [], None
+    try:
+        local = list(zip(mine, task_runner(mine)))
+    except Exception as exc:  # noqa: BLE001 - re-raised on every rank
+        err = f"{type(exc).__name__}: {exc}"
+    parts = _gather_checked(dist, world, local, err)
     scores: List[Optional[List[float]]] = [None] * n_tasks
     seen = 0
     for part in parts:
@@ -112,5 +163,37 @@ def cross_validate_distributed(ds, model: str = "cox", penalty: str = "l1",
     out["tasks_per_rank"] = len(mine)
     if final_fit:
         out["final_fit"] = survscan.fit(ds, model=model, penalty=penalty,
-                                        strength=out["selected"], tol=tol, max_cycles=max_cycles)
+                                        strength=out["selected"], tol=tol, max_cycles=max_cycles,
+                                        device=dev)
     return out
+
+
+def bootstrap_distributed(ds, model: str, penalty: str, strength: float, coefficient: int = 0,
+                          resamples: int = 200, seed: int = 0, tol: float = 1e-6,
+                          max_cycles: int = 1000, device: Optional[int] = None,
+                          draw_runner=None):
+    """bootstrap_interval (src/crossval.cpp:218-257) with the resamples dealt
+    round-robin over ranks (each rank's fits batched on its GPU), draws
+    gathered and merged in resample order: the interval equals the
+    single-process one for any world size."""
+    dist, rank, world = _dist()
+    import survscan
+    if resamples < 100:
+        raise ValueError("bootstrap needs at least 100 resamples")
+    dev = local_device() if device is None else device
+    mine = shard_tasks(resamples, rank, world)
+    if draw_runner is None:
+        def draw_runner(ids):
+            return list(survscan.bootstrap_run(ds, model, penalty, strength, [], coefficient,
+                                               list(ids), seed, tol, max_cycles, [dev]))
+    local, err = [], None
+    try:
+        local = list(zip(mine, draw_runner(mine)))
+    except Exception as exc:  # noqa: BLE001
+        err = f"{type(exc).__name__}: {exc}"
+    parts = _gather_checked(dist, world, local, err)
+    draws = [None] * resamples
+    for part in parts:
+        for b, v in part:
+            draws[b] = v
+    return survscan.bootstrap_merge(draws, resamples)

@@ -93,6 +93,39 @@ def test_bootstrap_interval(ss, fg):
     assert lo <= hi and failed == 0
 
 
+@pytest.mark.parametrize("name,model,lam,coef", [("cox_ties", "cox", 0.3, 2),
+                                                 ("fg_small", "finegray", 0.05, 1)])
+def test_bootstrap_parity_with_reference_module(ss, ref, name, model, lam, coef):
+    """bootstrap_interval (src/crossval.cpp:218-257): the same derive_seed
+    draw streams, the resamples' fits batched on the device (gss_fit_batch):
+    the interval equals the reference's within the coefficient tolerance."""
+    _, a, b = _both(ss, ref, name)
+    kw = dict(model=model, penalty="l1", strength=lam, coefficient=coef, resamples=120, seed=23,
+              tol=1e-10, max_cycles=500)
+    la, ha, fa = ss.bootstrap_interval(a, **kw)
+    lb, hb, fb = ref.bootstrap_interval(b, threads=1, **kw)
+    assert fa == fb
+    assert rel(la, lb) < TOL_BETA and rel(ha, hb) < TOL_BETA
+    # the per-resample draws, too (resample-ordered pieces of the rank driver)
+    draws = ss.bootstrap_run(a, model, "l1", lam, [], coef, list(range(120)), 23, 1e-10, 500)
+    assert tuple(ss.bootstrap_merge(draws, 120)) == (la, ha, fa)
+
+
+def test_drop_in_caller_runs(tmp_path):
+    """tests/cpp/drop_in_caller.cpp — written against the reference's C++
+    Engine / CCD API — runs on the device engine."""
+    import subprocess
+    from paper_2204_08183_b200 import build as B
+    host = os.path.join(ROOT, "paper_2204_08183_b200", "csrc", "host")
+    exe = str(tmp_path / "caller")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I" + host,
+                           os.path.join(ROOT, "tests", "cpp", "drop_in_caller.cpp"),
+                           "-L" + B.PKG, "-lsurvscan_b200", "-lgss", "-Wl,-rpath," + B.PKG,
+                           "-o", exe])
+    out = subprocess.check_output([exe], text=True)
+    assert "drop-in caller ok" in out
+
+
 def test_errors_surface(ss, fg):
     with pytest.raises(ss.SurvscanError):
         ss.fit(fg[0], model="cox")  # competing rows under a cox model
