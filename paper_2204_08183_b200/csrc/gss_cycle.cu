@@ -77,9 +77,7 @@ struct Geo {
   static constexpr uint32_t kOffL = kEBytes + kCBytes + kGBytes;
   static constexpr uint32_t kStage = (kOffL + 3 * kLBytes + 1023) / 1024 * 1024;
   static constexpr int kP = 1;            // producer warps (independent issue chains)
-  // consumers, control warp, producer(s), prep warp
-  static constexpr int kThreads = 32 * (kW + 1 + kP + 1);
-  static constexpr int kPrepWarp = kW + 1 + kP;
+  static constexpr int kThreads = 32 * (kW + 1 + kP);  // consumers, control warp, producer(s)
   static_assert(kStage % 1024 == 0, "stage alignment");
 };
 
@@ -165,18 +163,12 @@ struct Tail {
   uint64_t empty[S];
   StageInfo info[S];
   static constexpr int NG = Geo<FG>::kNG, GW = Geo<FG>::kGW;
-  // per-stage column bitmasks per 8-row thread-row, built by the prep warp
-  // before the consumers take the stage: xm = scan column (+ the first list
-  // entry's index << 8, valued columns), xn = next column (fused records)
-  uint32_t xm[S][256];
-  uint32_t xn[S][256];
-  // group exchange buffers, double-buffered by the group's tile parity (the
-  // group's warps run at most one barrier apart)
-  double gx[NG][2][GW][8];  // per-warp pass-group totals
-  double gr[NG][GW][10];    // per-warp record partials (non-fused records)
-  double gc[NG][2][16];     // the tile's carries
-  unsigned prepped;         // stream positions prepared (patched + masks) by the prep warp
-  unsigned slot_go;         // slots whose state the control warp has published
+  uint32_t xm[NG][2][256];  // per-group scan-column bitmask per thread-row (+ first-entry
+                            // offset), double-buffered by the group's tile parity
+  uint32_t xn[NG][2][256];  // per-group next-column bitmask (fused records)
+  double gx[NG][GW][8];  // per-warp pass-group totals (group exchange)
+  double gr[NG][GW][10]; // per-warp record partials (group exchange)
+  double gc[NG][16];     // the tile's carries (group exchange)
   double wpart[W][4];
   unsigned int progress[NG];
   SlotState ss;
@@ -499,23 +491,24 @@ __device__ __forceinline__ void producer(const CycleParams& P, unsigned char* sm
       const unsigned qw = q0 + static_cast<unsigned>(i) * NP;
       if (qw >= total) break;
       const int s = static_cast<int>(qw % S);
+      const int tl_i = __shfl_sync(0xffffffffu, tloc, i);
       if (lane == 0) {
         tl->mark[16 + s] = 0xA0u | (qw << 8);
         trace_c0(P, 24, static_cast<int>(qw));
         mbar_wait_wd(&tl->empty[s], ((qw / S) & 1u) ^ 1u, "producer empty-stage wait", qw, tl->mark);
         trace_c0(P, 25, static_cast<int>(qw));
         // the same tile of the previous slot must have committed its pending
-        // update (the prep warp fenced generic -> async proxy before
-        // publishing the position)
+        // update (the committing group fenced generic -> async proxy before
+        // publishing its progress)
         if (qw >= utc) {
           const unsigned prevq = qw - utc;
-          const unsigned* pr = &tl->prepped;
+          const unsigned* pr = &tl->progress[tl_i % G::kNG];
           if (flag_acquire(pr) < prevq + 1) {
             const unsigned long long tw = gtimer();
             while (flag_acquire(pr) < prevq + 1) {
               __nanosleep(32);
               if (gtimer() - tw > kWatchdogNs)
-                watchdog_trap("producer commit wait", qw, flag_acquire(pr), tl->mark);
+                watchdog_trap("producer progress wait", qw, flag_acquire(pr), tl->mark);
             }
           }
         }
@@ -594,9 +587,9 @@ __device__ __forceinline__ void group_sync(int g) {
 // both columns), so the tile totals ARE the record.
 template <bool FG, bool IND, int KIND, bool FUSED = false>
 __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl, unsigned char* sb,
-                                             int sidx, const StageInfo& inf, const SlotState& ss,
-                                             int g, int gw, int lane, int par, double& acc0,
-                                             double& acc1, int& bad, unsigned q) {
+                                             const StageInfo& inf, const SlotState& ss, int g,
+                                             int gw, int lane, int par, double& acc0,
+                                             double& acc1, int& bad, uint64_t* empty_bar) {
   using G = Geo<FG>;
   constexpr int GW = G::kGW, PPW = kPasses / GW, GT = 32 * GW;
   constexpr int NF = (KIND == kSlotLoglik) ? 1 : (IND ? 2 : 3);
@@ -616,23 +609,71 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   const ListRef& Lp = inf.l[0];
   const ListRef& Lc = inf.l[1];
   const ListRef& Ln = inf.l[2];
-  const uint32_t* xm = tl->xm[sidx];
-  const uint32_t* xn = tl->xn[sidx];
+  uint32_t* xm = tl->xm[g][par];
+  uint32_t* xn = tl->xn[g][par];
+  {  // the other buffers served the group's previous tile (released): clear them
+    uint32_t* om = tl->xm[g][par ^ 1];
+    uint32_t* on = tl->xn[g][par ^ 1];
+    for (int i = gt; i < 256; i += GT) {
+      om[i] = 0u;
+      on[i] = 0u;
+    }
+  }
   const bool has_cur = KIND == kSlotGrad && ss.col >= 0;
 
-  // ---- tile carries -> group smem (read after the group barrier) ----
-  if (gw == 0 && lane < (FG ? 15 : 7))
-    tl->gc[g][par][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
-  const double* tcv = tl->gc[g][par];
+  // ---- tile carries -> group smem (visible after the first group barrier) ----
+  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
+  const double* tcv = tl->gc[g];
 
-  // ---- stale tile after a refresh: reload exp(eta) from global (rare) ----
-  // (otherwise the prep warp has already patched + committed the pending
-  // update and built the stage's column masks)
+  // ---- stale tile after a refresh: reload exp(eta) from global ----
   if (ss.refresh) {
     for (int i = gt; i < kTileRows; i += GT) *e_at(sb, i) = __ldcg(P.e + row0 + i);
-    group_sync<FG>(g);
+  } else if (ss.pcol >= 0) {
+    // ---- patch + commit the pending update (src/engine.cpp:192-215) ----
+    for (int i = gt; i < Lp.cnt; i += GT) {
+      const int32_t r = list_at(lp, Lp, P.row_idx, i);
+      const int lr = static_cast<int>(r - row0);
+      if (code_at(sc, lr) & kCodeMasked) continue;
+      double* pe = e_at(sb, lr);
+      double en;
+      if (ss.pind) {
+        en = __dmul_rn(*pe, ss.phi);
+        red_add_f64(P.eta + r, ss.delta);  // xbeta_[i] += 1.0 * delta, fire-and-forget
+      } else {
+        const double ne = __dadd_rn(__ldcg(P.eta + r), __dmul_rn(P.vals[Lp.lo + i], ss.delta));
+        en = exp(ne);
+        P.eta[r] = ne;
+      }
+      *pe = en;
+      if constexpr (FG)  // L2 atomic store: measured 2% faster for Fine-Gray, not for Cox
+        atomicExch(reinterpret_cast<unsigned long long*>(P.e + r),
+                   static_cast<unsigned long long>(__double_as_longlong(en)));
+      else
+        P.e[r] = en;
+    }
+  }
+  // ---- scan-column bitmask per thread-row (xm is all-zero on entry) ----
+  if (has_cur) {
+    for (int i = gt; i < Lc.cnt; i += GT) {
+      const int32_t r = list_at(lcur, Lc, P.row_idx, i);
+      const int lr = static_cast<int>(r - row0);
+      uint32_t w = 1u << (lr & 7);
+      if (!IND) {
+        const bool first =
+            i == 0 || ((list_at(lcur, Lc, P.row_idx, i - 1) - row0) >> 3) != (lr >> 3);
+        if (first) w |= static_cast<uint32_t>(i) << 8;
+      }
+      atomicOr(&xm[lr >> 3], w);
+    }
+  }
+  if constexpr (FUSED) {
+    for (int i = gt; i < Ln.cnt; i += GT) {
+      const int lr = static_cast<int>(list_at(lnext, Ln, P.row_idx, i) - row0);
+      atomicOr(&xn[lr >> 3], 1u << (lr & 7));
+    }
   }
   mark<FG>(tl, 0x11u | (static_cast<unsigned>(t & 0xffff) << 8));
+  group_sync<FG>(g);
   trace_w0(P, 10, t);
 
   // per-row lane values of thread-row tr
@@ -763,7 +804,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   }
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < L; ++i) tl->gx[g][par][gw][i] = wt.v[i];
+    for (int i = 0; i < L; ++i) tl->gx[g][gw][i] = wt.v[i];
   }
   const unsigned wany = __reduce_or_sync(0xffffffffu, work);
   mark<FG>(tl, 0x12u | (static_cast<unsigned>(t & 0xffff) << 8));
@@ -776,26 +817,12 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   for (int w2 = 0; w2 < GW; ++w2) {
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      const double x = tl->gx[g][par][w2][i];
+      const double x = tl->gx[g][w2][i];
       if (w2 < gw) off.v[i] = __dadd_rn(off.v[i], x);
       ttot.v[i] = __dadd_rn(ttot.v[i], x);
     }
   }
   trace_w0(P, 11, t);
-  if constexpr (FUSED) {
-    // the next slot's record = the tile totals of the two extra lanes; publish
-    // it (and the tile's progress) before the transform
-    if (gw == 0 && lane == 0) {
-      double* rec = rec_at<FG>(P, tl, t, inf.li);
-      rec[kRa] = ttot.v[0];
-      rec[kRb] = ttot.v[NF];
-      rec[kRc] = ttot.v[NF];
-      rec[kRsa] = ttot.v[1];  // indicator scan column: its b lane is sum e over its rows
-      rec[kRsb] = ttot.v[NF + 1];
-      rec[kRsc] = ttot.v[NF + 1];
-      flag_release(&tl->progress[g], q + 1);
-    }
-  }
 
   // ---- phase 3: transform at tied-block ends (Breslow), passes with work only ----
   if (wany) {
@@ -878,6 +905,15 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
 
   // ---- the next slot's per-tile record (from the patched staged tile) ----
   if constexpr (FUSED) {
+    if (gw == 0 && lane == 0) {
+      double* rec = rec_at<FG>(P, tl, t, inf.li);
+      rec[kRa] = ttot.v[0];
+      rec[kRb] = ttot.v[NF];
+      rec[kRc] = ttot.v[NF];
+      rec[kRsa] = ttot.v[1];  // indicator scan column: its b lane is sum e over its rows
+      rec[kRsb] = ttot.v[NF + 1];
+      rec[kRsc] = ttot.v[NF + 1];
+    }
   } else if (!(P.dbg & 2)) {
     double rb = 0.0, rc = 0.0, rsa = 0.0, rsb = 0.0, rsc = 0.0;
     double rub = 0.0, ruc = 0.0, rusa = 0.0, rusb = 0.0, rusc = 0.0;
@@ -940,7 +976,6 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   }
   mark<FG>(tl, 0x13u | (static_cast<unsigned>(t & 0xffff) << 8));
   if constexpr (!FUSED) group_sync<FG>(g);
-  if (!FUSED && gw == 0 && lane == 0 && (P.dbg & 2)) flag_release(&tl->progress[g], q + 1);
   if (!FUSED && gw == 0 && lane == 0 && !(P.dbg & 2)) {
     constexpr int NR = FG ? 10 : 5;
     double s[NR];
@@ -965,147 +1000,30 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       rec[kRusb] = s[8];
       rec[kRusc] = s[9];
     }
-    flag_release(&tl->progress[g], q + 1);  // the tile's record before its progress
   }
   trace_w0(P, 13, t);
 }
 
+// returns true if the stage was already released (fused path)
 template <bool FG>
-__device__ __forceinline__ void consume_tile(const CycleParams& P, Tail<FG>* tl, unsigned char* sb,
-                                             int sidx, const StageInfo& inf, const SlotState& ss,
-                                             int g, int gw, int lane, int par, double& acc0,
-                                             double& acc1, int& bad, unsigned q) {
+__device__ __forceinline__ bool consume_tile(const CycleParams& P, Tail<FG>* tl, unsigned char* sb,
+                                             const StageInfo& inf, const SlotState& ss, int g,
+                                             int gw, int lane, int par, double& acc0,
+                                             double& acc1, int& bad, uint64_t* empty_bar) {
   if constexpr (!FG) {
     if (ss.fused) {
-      process_tile<false, true, kSlotGrad, true>(P, tl, sb, sidx, inf, ss, g, gw, lane, par, acc0,
-                                                 acc1, bad, q);
-      return;
+      process_tile<false, true, kSlotGrad, true>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1,
+                                                 bad, empty_bar);
+      return false;
     }
   }
   if (ss.kind == kSlotLoglik)
-    process_tile<FG, true, kSlotLoglik>(P, tl, sb, sidx, inf, ss, g, gw, lane, par, acc0, acc1,
-                                        bad, q);
+    process_tile<FG, true, kSlotLoglik>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
   else if (ss.cind)
-    process_tile<FG, true, kSlotGrad>(P, tl, sb, sidx, inf, ss, g, gw, lane, par, acc0, acc1, bad,
-                                      q);
+    process_tile<FG, true, kSlotGrad>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
   else
-    process_tile<FG, false, kSlotGrad>(P, tl, sb, sidx, inf, ss, g, gw, lane, par, acc0, acc1,
-                                       bad, q);
-}
-
-// ---------------------------------------------------------------------------
-// prep warp: for every stream position, in order, once its stage landed and
-// the control warp published the slot's state: patch + commit the pending
-// update into the staged tile (src/engine.cpp:192-215) and build the stage's
-// column bitmasks, then publish the position (consumers take it, and the
-// producer may reload the same tile for the next slot: the update is
-// committed).  Off the consumers' critical path.
-// ---------------------------------------------------------------------------
-template <bool FG>
-__device__ __forceinline__ void prep_warp(const CycleParams& P, unsigned char* smem, Tail<FG>* tl,
-                                          int tc) {
-  using G = Geo<FG>;
-  constexpr int S = G::kS;
-  const int lane = threadIdx.x & 31;
-  const unsigned total = static_cast<unsigned>(P.nslots) * static_cast<unsigned>(tc);
-  const SlotState& ss = tl->ss;
-  unsigned slot = 0, tloc = 0;
-  for (unsigned q = 0; q < total; ++q) {
-    const int s = static_cast<int>(q % S);
-    if (lane == 0) {
-      // the slot's state (pending update, columns) is published
-      if (flag_acquire(&tl->slot_go) <= slot) {
-        const unsigned long long tw = gtimer();
-        while (flag_acquire(&tl->slot_go) <= slot) {
-          __nanosleep(32);
-          if (gtimer() - tw > kWatchdogNs) watchdog_trap("prep slot wait", q, slot, tl->mark);
-        }
-      }
-      // the producer issued q (then the parity of the stage is unambiguous)
-      if (flag_acquire(&tl->issued) <= q) {
-        const unsigned long long tw = gtimer();
-        while (flag_acquire(&tl->issued) <= q) {
-          __nanosleep(32);
-          if (gtimer() - tw > kWatchdogNs) watchdog_trap("prep issue wait", q, slot, tl->mark);
-        }
-      }
-      mbar_wait_wd(&tl->full[s], (q / S) & 1u, "prep full-stage wait", q, tl->mark);
-    }
-    __syncwarp();
-    unsigned char* sb = smem + size_t(s) * G::kStage;
-    const StageInfo& inf = tl->info[s];
-    const bool dry = ss.dry != 0 || (P.dbg & 1);
-    uint32_t* xm = tl->xm[s];
-    uint32_t* xn = tl->xn[s];
-    for (int i = lane; i < 256; i += 32) {
-      xm[i] = 0u;
-      xn[i] = 0u;
-    }
-    __syncwarp();
-    if (!dry) {
-      const long long row0 = static_cast<long long>(inf.tile) * kTileRows;
-      const unsigned char* sc = sb + G::kOffC;
-      const int32_t* lbase = reinterpret_cast<const int32_t*>(sb + G::kOffL);
-      const ListRef& Lp = inf.l[0];
-      const ListRef& Lc = inf.l[1];
-      const ListRef& Ln = inf.l[2];
-      bool committed = false;
-      if (!ss.refresh && ss.pcol >= 0) {
-        // patch + commit the pending update
-        for (int i = lane; i < Lp.cnt; i += 32) {
-          const int32_t r = list_at(lbase, Lp, P.row_idx, i);
-          const int lr = static_cast<int>(r - row0);
-          if (code_at(sc, lr) & kCodeMasked) continue;
-          double* pe = e_at(sb, lr);
-          double en;
-          if (ss.pind) {
-            en = __dmul_rn(*pe, ss.phi);
-            red_add_f64(P.eta + r, ss.delta);  // xbeta_[i] += 1.0 * delta, fire-and-forget
-          } else {
-            const double ne =
-                __dadd_rn(__ldcg(P.eta + r), __dmul_rn(P.vals[Lp.lo + i], ss.delta));
-            en = exp(ne);
-            P.eta[r] = ne;
-          }
-          *pe = en;
-          if constexpr (FG)  // L2 atomic store: measured 2% faster for Fine-Gray, not for Cox
-            atomicExch(reinterpret_cast<unsigned long long*>(P.e + r),
-                       static_cast<unsigned long long>(__double_as_longlong(en)));
-          else
-            P.e[r] = en;
-          committed = true;
-        }
-      }
-      // scan-column bitmask per thread-row (+ first entry index, valued)
-      if (ss.kind == kSlotGrad && ss.col >= 0) {
-        const bool ind = ss.cind != 0;
-        for (int i = lane; i < Lc.cnt; i += 32) {
-          const int32_t r = list_at(lbase + G::kCap, Lc, P.row_idx, i);
-          const int lr = static_cast<int>(r - row0);
-          uint32_t w = 1u << (lr & 7);
-          if (!ind) {
-            const bool first = i == 0 || ((list_at(lbase + G::kCap, Lc, P.row_idx, i - 1) - row0) >> 3) !=
-                                             (lr >> 3);
-            if (first) w |= static_cast<uint32_t>(i) << 8;
-          }
-          atomicOr(&xm[lr >> 3], w);
-        }
-      }
-      if (!FG && ss.fused) {
-        for (int i = lane; i < Ln.cnt; i += 32) {
-          const int lr = static_cast<int>(list_at(lbase + 2 * G::kCap, Ln, P.row_idx, i) - row0);
-          atomicOr(&xn[lr >> 3], 1u << (lr & 7));
-        }
-      }
-      if (committed) fence_proxy_async_global();  // commits before the producer's TMA reload
-    }
-    __syncwarp();
-    if (lane == 0) flag_release(&tl->prepped, q + 1);
-    if (++tloc == static_cast<unsigned>(tc)) {
-      tloc = 0;
-      ++slot;
-    }
-  }
+    process_tile<FG, false, kSlotGrad>(P, tl, sb, inf, ss, g, gw, lane, par, acc0, acc1, bad, empty_bar);
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -1798,11 +1716,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     ss.fused = f.fused;
   };
   auto go = [&](int task) {
-    if (lane == 0) {
-      tl->task = task;
-      // the next slot's state is complete: the prep warp may patch its tiles
-      if (task == kTaskNext) flag_release(&tl->slot_go, flag_acquire(&tl->slot_go) + 1u);
-    }
+    if (lane == 0) tl->task = task;
     __syncwarp();
     bar_arrive_n(kBarGo, NB);
   };
@@ -2158,17 +2072,19 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&tl->full[s], 1);
-      mbar_init(&tl->empty[s], Gm::kGW);  // every warp of the consuming group arrives
+      mbar_init(&tl->empty[s], 1);
     }
     mbar_init(&tl->gbar, 1);
     tl->gphase = 0u;
     tl->issued = 0u;
-    tl->prepped = 0u;
-    tl->slot_go = 0u;
     fence_mbar_init();
   }
   if (tid < Gm::kNG) tl->progress[tid] = 0u;
   if (tid < 32) trace_slot(tid) = 0u;
+  for (int i = tid; i < Gm::kNG * 512; i += blockDim.x) {
+    (&tl->xm[0][0][0])[i] = 0u;
+    (&tl->xn[0][0][0])[i] = 0u;
+  }
   for (int i = tid; i < min(tc, MaxTc<FG>::v); i += blockDim.x) tl->tfirst[i] = P.tile_first[t0 + i];
   if (tid == 0) tl->task = kTaskNext;
   // static stratum flags of every CTA range (carry segmentation bounds)
@@ -2200,10 +2116,6 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     tl->ext_r = (P.ext && !fe) ? 1 : 0;
   }
 
-  if (warp == Gm::kPrepWarp) {
-    prep_warp<FG>(P, smem, tl, tc);
-    return;
-  }
   if (warp > W) {
     producer<FG>(P, smem, tl, t0, tc, &L.tm_e[f], &L.tm_code[f], &L.tm_g[f], warp - W - 1);
     return;
@@ -2248,32 +2160,39 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       for (int i = g; i < tc; i += NGr) {
         const unsigned q = qbase + static_cast<unsigned>(i);
         const int s = static_cast<int>(q % S);
-        // the prep warp handles positions in order, after the stage landed
-        // (and after the producer issued it, so no stage-parity aliasing)
+        const uint32_t ph = (q / S) & 1u;
+        // A parity wait only tells apart consecutive phases of a stage: a group
+        // that runs two ring cycles ahead of a slow group would see the phase
+        // of position q - 2S as "complete". Wait until the producer has issued
+        // q (it issues q only after q - S was released), then the parity test
+        // is exact.
         {
-          const unsigned* pp = &tl->prepped;
-          if (flag_acquire(pp) <= q) {
+          const unsigned* iss = &tl->issued;
+          if (flag_acquire(iss) <= q) {
             const unsigned long long tw = gtimer();
             unsigned it = 0;
-            while (flag_acquire(pp) <= q) {
+            while (flag_acquire(iss) <= q) {
               __nanosleep(32);
               if ((++it & 63u) == 0 && gtimer() - tw > kWatchdogNs)
-                watchdog_trap("consumer prep wait", q, flag_acquire(pp),
+                watchdog_trap("consumer issue wait", q, flag_acquire(iss),
                               lane == 0 ? tl->mark : nullptr);
             }
           }
         }
+        mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", q, lane == 0 ? tl->mark : nullptr);
         unsigned char* sb = smem + size_t(s) * Gm::kStage;
-        if (!dry && !(P.dbg & 1)) {
-          consume_tile<FG>(P, tl, sb, s, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1, bad, q);
-        } else if (gw == 0 && lane == 0) {
-          flag_release(&tl->progress[g], q + 1);
-        }
+        if (!dry && !(P.dbg & 1))
+          consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1, bad,
+                           &tl->empty[s]);
         gpar ^= 1;
+        if (ss.pcol >= 0 && !ss.refresh && (gw * 32 + lane) < tl->info[s].l[0].cnt)
+          fence_proxy_async_global();
         mark<FG>(tl, 0x15u | (q << 8));
-        // each warp releases the stage when done with it (empty[s] counts GW)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tl->empty[s]);
+        group_sync<FG>(g);
+        if (gw == 0 && lane == 0) {
+          flag_release(&tl->progress[g], q + 1);  // the tile's record before its progress
+          mbar_arrive(&tl->empty[s]);
+        }
       }
     }
     qbase += static_cast<unsigned>(tc);
