@@ -36,12 +36,25 @@ def _run(cmd):
 
 
 def build_libgss(force=False):
+    """Each .cu compiles to its own object (in parallel, only when it or a
+    shared header changed), then one link."""
+    from concurrent.futures import ThreadPoolExecutor
     cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "gss.h")]
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "gss.h")]
     extra = ["-DGSS_ENABLE_TRACE=1"] if os.environ.get("GSS_TRACE_BUILD") == "1" else []
-    if force or extra or _newer(LIBGSS, deps):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-diag-suppress", "177", *extra, "-shared", *cu, "-o", LIBGSS])
+    objdir = os.path.join(ROOT, "build", "obj" + ("_trace" if extra else ""))
+    os.makedirs(objdir, exist_ok=True)
+    objs, todo = [], []
+    for src in cu:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or _newer(obj, [src] + hdrs):
+            todo.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-diag-suppress", "177", *extra, "-c", src, "-o", obj])
+    with ThreadPoolExecutor(max(1, len(todo))) as ex:
+        list(ex.map(_run, todo))
+    if force or todo or _newer(LIBGSS, objs):
+        _run([NVCC, *ARCH, "-shared", *objs, "-o", LIBGSS])
     return LIBGSS
 
 
