@@ -26,8 +26,12 @@ CSC indices + 120 MB of per-row state) is far larger than L2.
           cores, timed per coordinate on a bounded sample of the same workload
           (N = 10M rows, 20 columns of 1% density, one cycle).
 
-Multi-GPU: a single fit does not shard at 1 GPU scale; --gpus N runs N
-independent replicas (one process per GPU, torchrun), "scaling": "weak".
+Multi-GPU: a single C2 fit fits one B200, so the primary `value` at --gpus N
+is N independent replicas (one process per GPU, torchrun), "scaling": "weak".
+The north star's multi-GPU workload, C4 cross-validation, is measured in the
+same run as secondary.c4_cv: its (grid point) tasks are dealt over the N ranks
+(no data-path collective) and time-to-result is the max over ranks, so the
+C4 scaling curve reads off secondary.c4_cv.time_to_result_s across N.
 """
 from __future__ import annotations
 
@@ -70,6 +74,9 @@ def parse():
     ap.add_argument("--c3-cycles", type=int, default=2)
     ap.add_argument("--no-parity", action="store_true", help="skip the C2 oracle spot-check")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 time-to-fit pair")
+    ap.add_argument("--c4", type=int, default=1, help="C4 cross-validation measurement (0 = skip)")
+    ap.add_argument("--c4-n", type=int, default=1_000_000)
+    ap.add_argument("--c4-p", type=int, default=1000)
     return ap.parse_args()
 
 
@@ -416,6 +423,7 @@ def run_gss(args, dist):
         e2e_cycles.append(r2["cycles"])
         del e2, d2
     c3 = run_c3(args, dist) if args.c3_p > 0 else None
+    c4 = run_c4(args, dist) if args.c4 else None
     c1 = run_c1(dist) if (dist.rank == 0 and not args.no_c1) else None
     out = {
         "metric": "cox_ccd_coordinate_updates_per_s",
@@ -458,6 +466,8 @@ def run_gss(args, dist):
         out["secondary"]["c3_finegray"] = c3
     if c1 is not None:
         out["secondary"]["c1_time_to_fit"] = c1
+    if c4 is not None:
+        out["secondary"]["c4_cv"] = c4
     return out
 
 
@@ -490,6 +500,59 @@ def run_c3(args, dist):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_coordinate": round(per_coord, 1)}}
+
+
+def run_c4(args, dist):
+    """Config C4 (stratified Cox, 10-fold CV x 20-point lambda grid, N=1e6,
+    p=1000, 100 strata) through the drop-in survscan API; the (grid point)
+    tasks are dealt over the ranks (one GPU each), time-to-result = max over
+    ranks.  Beside it, the same bounded CV sample (unstratified: the reference
+    has no strata; 1 grid point, 10 folds, 2 cycles per fold fit) through the
+    GPU path and through the unmodified reference on this box's host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import c4_cv
+    import survscan
+    out = c4_cv.run(args.c4_n, args.c4_p, 100, 20, 10, device=dist.local,
+                    barrier=dist.barrier, reduce_max=dist.max)
+    out["n_gpus"] = dist.world
+    out["scaling"] = "weak (CV tasks dealt over ranks; no data-path collective)"
+    if dist.rank != 0:
+        return out
+    # bounded side-by-side sample, same data and folds on both paths
+    try:
+        from paper_2204_08183_b200 import capi
+        sim = capi.SimData(args.c4_n, args.c4_p, 0.01, 0.8, 4, 0.9, 1000.0, device=dist.local)
+        cols = np.repeat(np.arange(args.c4_p, dtype=np.int64), np.diff(sim.col_ptr))
+        rows = np.asarray(sim.row_idx, np.int64)
+        obs = (np.asarray(sim.times), np.asarray(sim.status, np.int64), rows, cols,
+               np.ones(len(rows)), args.c4_p)
+        gds = survscan.dataset_from_coo(*obs)
+        lam = [survscan.gamma_max(gds, "cox") / 10.0]
+        kw = dict(model="cox", penalty="l1", grid=lam, folds=10, repetitions=1, seed=7,
+                  max_cycles=2)
+        survscan.cross_validate(gds, devices=[dist.local], **kw)  # warm
+        t0 = time.perf_counter()
+        g = survscan.cross_validate(gds, devices=[dist.local], **kw)
+        gpu_s = time.perf_counter() - t0
+        ref = reference_module()
+        rds = ref.dataset_from_coo(*obs)
+        threads = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        r = ref.cross_validate(rds, threads=threads, **kw)
+        ref_s = time.perf_counter() - t0
+        out["sample"] = {"what": "cross_validate, unstratified, grid=[gamma_max/10], 10 folds, "
+                                 "1 repetition, max_cycles=2 per fold fit, + final refit",
+                         "gpu_seconds": round(gpu_s, 3), "reference_seconds": round(ref_s, 3),
+                         "reference_cores": threads, "speedup": round(ref_s / gpu_s, 2),
+                         "same_selection": bool(abs(g["selected"] - r["selected"]) <= 1e-12 *
+                                                abs(r["selected"])),
+                         "max_rel_diff_final_beta": float(np.max(
+                             np.abs(np.asarray(g["final_fit"]["beta"]) -
+                                    np.asarray(r["final_fit"]["beta"])) /
+                             np.maximum(1.0, np.abs(np.asarray(r["final_fit"]["beta"])))))}
+    except Exception as exc:  # pragma: no cover - reference module missing on the box
+        out["sample"] = {"unavailable": str(exc)[:200]}
+    return out
 
 
 def main():

@@ -87,6 +87,24 @@ int gss_device_count(void);
  */
 int gss_dataset_pack(const gss_host_dataset* host, int device, gss_dataset** out);
 void gss_dataset_release(gss_dataset* ds);
+
+/*
+ * Device ingestion (sort_and_block / dataset_from_coo, src/dataset.cpp:190-262):
+ * orders the rows by (stratum asc,) time desc, row id asc and builds the CSC
+ * over sorted positions with CUB radix sorts on `device`.
+ *   order_out[n]     sorted position -> input row id
+ *   col_ptr_out[p+1], row_pos_out[nnz], vals_out[nnz] (capacity nnz): CSC of
+ *                    the nonzero cells (zero values are absent cells)
+ *   *nnz_out         stored cells
+ *   err_info[2]      on GSS_ERR_INDEX / GSS_ERR_DOMAIN: [0] = first failing
+ *                    input entry; on GSS_ERR_DUPLICATE: [0] sorted position,
+ *                    [1] column of the first repeated cell
+ * strata may be NULL.  n and nnz must be below 2^31 per call.
+ */
+int gss_coo_sort(int device, int64_t n, const double* times, const int64_t* strata, int64_t nnz,
+                 const int64_t* rows, const int64_t* cols, const double* vals, int64_t p,
+                 int64_t* order_out, int64_t* col_ptr_out, int32_t* row_pos_out, double* vals_out,
+                 int64_t* nnz_out, int64_t* err_info);
 /* Bytes of device memory held by the packed dataset. */
 int64_t gss_dataset_device_bytes(const gss_dataset* ds);
 

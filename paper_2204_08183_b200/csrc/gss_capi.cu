@@ -31,6 +31,9 @@
 #include "gss_device.cuh"
 #include "gss_kernels.cuh"
 
+namespace gss {
+int set_last_error(int code, const std::string& msg);
+}
 using namespace gss;
 
 namespace {
@@ -56,6 +59,12 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace
+
+// shared with the other C-ABI translation units (gss_ingest.cu)
+int gss::set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
 
 #define GSS_CUDA(call)                                                                  \
   do {                                                                                  \

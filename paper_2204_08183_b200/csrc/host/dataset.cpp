@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <charconv>
 #include <cstdio>
+#include <cstdlib>
 #include <string_view>
 #include <unordered_set>
 #include <cmath>
@@ -13,6 +14,7 @@
 #include <sstream>
 
 #include "../../../include/gss.h"
+#include "survscan/engine.hpp"  // default_device()
 #include "survscan/errors.hpp"
 
 namespace survscan {
@@ -64,6 +66,28 @@ SurvivalDataset SurvivalDataset::assemble(
       ds.row_idx_.push_back(static_cast<std::int32_t>(i));
       ds.vals_.push_back(v);
     }
+  ds.dev_ = std::make_shared<DeviceCache>();
+  return ds;
+}
+
+SurvivalDataset SurvivalDataset::assemble_csc(std::vector<double> times, std::vector<int> status,
+                                              std::vector<std::int64_t> row_ids,
+                                              std::vector<std::int64_t> col_ptr,
+                                              std::vector<std::int32_t> row_idx,
+                                              std::vector<double> vals,
+                                              std::vector<std::uint8_t> stratum_start) {
+  SurvivalDataset ds;
+  ds.times_ = std::move(times);
+  ds.status_ = std::move(status);
+  ds.row_ids_ = std::move(row_ids);
+  ds.stratum_start_ = std::move(stratum_start);
+  for (int s : ds.status_) {
+    if (s == 1) ++ds.n_events_;
+    if (s == 2) ds.has_competing_ = true;
+  }
+  ds.col_ptr_ = std::move(col_ptr);
+  ds.row_idx_ = std::move(row_idx);
+  ds.vals_ = std::move(vals);
   ds.dev_ = std::make_shared<DeviceCache>();
   return ds;
 }
@@ -191,6 +215,51 @@ SurvivalDataset dataset_from_coo(const std::vector<double>& times, const std::ve
       throw DomainError("observation time must be finite and >= 0");
     if (status[i] != 0 && status[i] != 1 && status[i] != 2)
       throw DomainError("status must be 0, 1 or 2");
+  }
+  // Device ingestion when a GPU is present (gss_coo_sort: CUB radix sorts,
+  // same order, same first-error semantics); SURVSCAN_HOST_INGEST=1 forces
+  // the host sort below.
+  if (gss_device_count() > 0 && !std::getenv("SURVSCAN_HOST_INGEST")) {
+    const std::size_t k = rows.size();
+    std::vector<std::int64_t> order(n), col_ptr(n_cols + 1);
+    std::vector<std::int32_t> rp(k);
+    std::vector<double> vv(k);
+    std::int64_t m = 0, err[2] = {-1, -1};
+    const int rc = gss_coo_sort(default_device(), static_cast<std::int64_t>(n), times.data(),
+                                strata.empty() ? nullptr : strata.data(),
+                                static_cast<std::int64_t>(k), rows.data(), cols.data(),
+                                values.data(), static_cast<std::int64_t>(n_cols), order.data(),
+                                col_ptr.data(), rp.data(), vv.data(), &m, err);
+    if (rc == GSS_ERR_INDEX || (rc == GSS_ERR_DOMAIN && err[0] >= 0)) {
+      const std::size_t e = static_cast<std::size_t>(err[0]);
+      if (rows[e] < 0 || static_cast<std::size_t>(rows[e]) >= n)
+        throw IndexError("matrix row " + std::to_string(rows[e]) + " outside [0, " +
+                         std::to_string(n) + ")");
+      if (cols[e] < 0 || static_cast<std::size_t>(cols[e]) >= n_cols)
+        throw IndexError("matrix column " + std::to_string(cols[e]) + " outside [0, " +
+                         std::to_string(n_cols) + ")");
+      throw DomainError("matrix value must be finite");
+    }
+    if (rc == GSS_ERR_DUPLICATE)
+      throw DuplicateEntryError("matrix cell (" + std::to_string(order[err[0]]) + ", " +
+                                std::to_string(err[1]) + ") appears more than once");
+    check(rc);
+    std::vector<double> t(n);
+    std::vector<int> s(n);
+    std::vector<std::uint8_t> ss;
+    if (!strata.empty()) ss.assign(n, 0);
+    for (std::size_t i = 0; i < n; ++i) {
+      const std::size_t o = static_cast<std::size_t>(order[i]);
+      t[i] = times[o];
+      s[i] = status[o];
+      if (!strata.empty())
+        ss[i] = (i == 0 || strata[o] != strata[static_cast<std::size_t>(order[i - 1])]) ? 1 : 0;
+    }
+    rp.resize(static_cast<std::size_t>(m));
+    vv.resize(static_cast<std::size_t>(m));
+    return SurvivalDataset::assemble_csc(std::move(t), std::move(s), std::move(order),
+                                         std::move(col_ptr), std::move(rp), std::move(vv),
+                                         std::move(ss));
   }
   // (stratum asc,) time desc, row id asc
   std::vector<std::size_t> order(n);

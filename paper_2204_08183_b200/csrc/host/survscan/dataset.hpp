@@ -75,6 +75,12 @@ class SurvivalDataset {
   gss_dataset* device(int device) const;
 
   // Build from sorted observations + per-column (position, value) lists.
+  // sorted layout already in CSC form (device ingestion, gss_coo_sort)
+  static SurvivalDataset assemble_csc(std::vector<double> times, std::vector<int> status,
+                                      std::vector<std::int64_t> row_ids,
+                                      std::vector<std::int64_t> col_ptr,
+                                      std::vector<std::int32_t> row_idx, std::vector<double> vals,
+                                      std::vector<std::uint8_t> stratum_start = {});
   static SurvivalDataset assemble(std::vector<double> times, std::vector<int> status,
                                   std::vector<std::int64_t> row_ids, std::size_t n_cols,
                                   std::vector<std::vector<std::pair<std::uint32_t, double>>> cols,
