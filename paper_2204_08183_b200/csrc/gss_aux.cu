@@ -64,6 +64,19 @@ __global__ void colmax_kernel(const int64_t* __restrict__ col_ptr, const double*
   }
 }
 
+__global__ void fill_dense_kernel(const int64_t* __restrict__ col_ptr, const int32_t* __restrict__ row_idx,
+                                  const double* __restrict__ vals, const int32_t* __restrict__ slot,
+                                  int64_t p, int64_t npad, double* __restrict__ pool) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; j < p;
+       j += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    if (slot[j] < 0) continue;
+    double* col = pool + size_t(slot[j]) * size_t(npad);
+    for (int64_t k = col_ptr[j] + lane; k < col_ptr[j + 1]; k += 32)
+      col[row_idx[k]] = vals ? vals[k] : 1.0;
+  }
+}
+
 __global__ void csr_count_kernel(const int32_t* __restrict__ row_idx, int64_t nnz,
                                  int64_t* __restrict__ cnt) {
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
@@ -259,6 +272,15 @@ cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s) {
   tile_ptr_kernel<<<grid_for(p * (ntiles + 1), 256), 256, 0, s>>>(col_ptr, row_idx, p, ntiles,
                                                                    tile_ptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_dense(const int64_t* col_ptr, const int32_t* row_idx, const double* vals,
+                              const int32_t* slot, int64_t p, int64_t npad, double* pool,
+                              cudaStream_t s) {
+  if (p == 0) return cudaSuccess;
+  fill_dense_kernel<<<grid_for(p * 32, 256), 256, 0, s>>>(col_ptr, row_idx, vals, slot, p, npad,
+                                                          pool);
   return cudaGetLastError();
 }
 

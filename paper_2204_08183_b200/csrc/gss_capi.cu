@@ -140,6 +140,9 @@ struct gss_dataset {
   double* csr_val = nullptr;
   double* colmax = nullptr;
   uint8_t* tile_first = nullptr;
+  int32_t* dense_idx = nullptr;      // [p] dense-pool slot or -1 (density >= 25%)
+  double* dense_pool = nullptr;      // [ndense][npad]
+  int64_t ndense = 0;
   int64_t bytes = 0;
   std::vector<int64_t> h_col_ptr;
 
@@ -149,7 +152,7 @@ struct gss_dataset {
     cudaSetDevice(device);
     for (void* q : {(void*)col_ptr, (void*)row_idx, (void*)vals, (void*)col_ind, (void*)tile_ptr,
                     (void*)row_ptr, (void*)csr_col, (void*)csr_val, (void*)colmax,
-                    (void*)tile_first})
+                    (void*)tile_first, (void*)dense_idx, (void*)dense_pool})
       if (q) cudaFree(q);
     if (prev >= 0) cudaSetDevice(prev);
   }
@@ -610,6 +613,27 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
     PK(launch_colmax(ds->col_ptr, ds->has_vals ? ds->vals : nullptr, p, ds->colmax, s));
   }
+  // Dense columns (density >= 25%: the reference stores them as dense arrays,
+  // SparseColumn::make src/dataset.cpp:126-157): values by device position in
+  // a pool the cycle kernel reads row-wise instead of their tile index lists.
+  if (p) {
+    Nvtx nv("pack: dense columns");
+    std::vector<int32_t> slot(static_cast<size_t>(p), -1);
+    for (int64_t j = 0; j < p; ++j) {
+      const int64_t cnt = ds->h_col_ptr[j + 1] - ds->h_col_ptr[j];
+      if (n && double(cnt) / double(n) >= 0.25) slot[j] = static_cast<int32_t>(ds->ndense++);
+    }
+    PK(dalloc(&ds->dense_idx, p));
+    PK(cudaMemcpyAsync(ds->dense_idx, slot.data(), p * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if (ds->ndense) {
+      PK(dalloc(&ds->dense_pool, ds->ndense * npad));
+      PK(cudaMemsetAsync(ds->dense_pool, 0, ds->ndense * npad * sizeof(double), s));
+      PK(launch_fill_dense(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr,
+                           ds->dense_idx, p, npad, ds->dense_pool, s));
+      ds->bytes += ds->ndense * npad * 8;
+    }
+    ds->bytes += p * 4;
+  }
   // CSR transpose over device positions: count -> exclusive scan -> fill -> per-row sort
   {
     Nvtx nv("pack: csr transpose");
@@ -759,6 +783,8 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.vals = ds->vals;
   P.col_ind = ds->col_ind;
   P.tile_ptr = ds->tile_ptr;
+  P.dense_idx = ds->dense_idx;
+  P.dense_pool = ds->dense_pool;
   P.row_ptr = ds->row_ptr;
   P.csr_col = ds->csr_col;
   P.csr_val = ds->csr_val;

@@ -95,6 +95,7 @@ struct StageInfo {
 struct SlotState {
   long long col;   // scan column of the slot (-1: log-likelihood slot)
   long long pcol;  // pending-update column (-1: none)
+  long long ncol;  // next slot's column (-1: none / objective)
   double delta, phi;
   int pind;        // pending column is an indicator column
   int cind;        // scan column is an indicator column
@@ -108,7 +109,7 @@ struct SlotState {
 };
 
 struct SlotFields {
-  long long col;
+  long long col, ncol;
   int kind, cind, nind, fused, valid;
 };
 
@@ -620,6 +621,16 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     }
   }
   const bool has_cur = KIND == kSlotGrad && ss.col >= 0;
+  // dense columns (density >= 25%, SparseColumn::make src/dataset.cpp:126-157):
+  // values by row from the dense pool instead of the tile's index list
+  auto dense_of = [&](long long c) -> const double* {
+    if (c < 0 || !P.dense_idx) return nullptr;
+    const int k = P.dense_idx[c];
+    return k < 0 ? nullptr : P.dense_pool + size_t(k) * size_t(P.npad);
+  };
+  const double* dcur = (!IND && has_cur) ? dense_of(ss.col) : nullptr;
+  const double* dpen = (ss.pcol >= 0 && !ss.pind) ? dense_of(ss.pcol) : nullptr;
+  const double* dnxt = ss.nind ? nullptr : dense_of(ss.ncol);
 
   // ---- tile carries -> group smem (visible after the first group barrier) ----
   if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
@@ -628,6 +639,22 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   // ---- stale tile after a refresh: reload exp(eta) from global ----
   if (ss.refresh) {
     for (int i = gt; i < kTileRows; i += GT) *e_at(sb, i) = __ldcg(P.e + row0 + i);
+  } else if (dpen) {
+    // ---- dense pending column: own rows, e = exp(eta + x*delta) ----
+    for (int lr = gt; lr < kTileRows; lr += GT) {
+      const double x = __ldg(dpen + row0 + lr);
+      if (x == 0.0 || (code_at(sc, lr) & kCodeMasked)) continue;
+      const long long r = row0 + lr;
+      const double ne = __dadd_rn(__ldcg(P.eta + r), __dmul_rn(x, ss.delta));
+      const double en = exp(ne);
+      P.eta[r] = ne;
+      *e_at(sb, lr) = en;
+      if constexpr (FG)
+        atomicExch(reinterpret_cast<unsigned long long*>(P.e + r),
+                   static_cast<unsigned long long>(__double_as_longlong(en)));
+      else
+        P.e[r] = en;
+    }
   } else if (ss.pcol >= 0) {
     // ---- patch + commit the pending update (src/engine.cpp:192-215) ----
     for (int i = gt; i < Lp.cnt; i += GT) {
@@ -653,7 +680,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     }
   }
   // ---- scan-column bitmask per thread-row (xm is all-zero on entry) ----
-  if (has_cur) {
+  if (has_cur && !dcur) {
     for (int i = gt; i < Lc.cnt; i += GT) {
       const int32_t r = list_at(lcur, Lc, P.row_idx, i);
       const int lr = static_cast<int>(r - row0);
@@ -717,6 +744,19 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     if constexpr (KIND == kSlotGrad) {
       if (has_cur) R.xb = xm[tr];
       if constexpr (!IND) {
+        if (dcur) {  // dense scan column: the thread-row's values, coalesced
+#pragma unroll
+          for (int c = 0; c < kIpt / 2; ++c) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(dcur + row0 + tr * kIpt) + c);
+            R.xv[2 * c] = v.x;
+            R.xv[2 * c + 1] = v.y;
+          }
+          uint32_t bits = 0;
+#pragma unroll
+          for (int m = 0; m < kIpt; ++m) bits |= (R.xv[m] != 0.0 ? 1u : 0u) << m;
+          R.xb = bits;
+          return;
+        }
         const uint32_t bits = R.xb & 0xffu;
         const long long k0 = Lc.lo + (R.xb >> 8);
         int k = 0;
@@ -919,11 +959,23 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     double rub = 0.0, ruc = 0.0, rusa = 0.0, rusb = 0.0, rusc = 0.0;
     const bool n_ind = ss.nind != 0;
     const bool ccd_cur = P.mode == kModeCcd && has_cur;
-    for (int i = gt; i < Ln.cnt; i += GT) {
-      const int32_t r = list_at(lnext, Ln, P.row_idx, i);
-      const int lr = static_cast<int>(r - row0);
+    auto in_cur = [&](int lr) {
+      return dcur ? (__ldg(dcur + row0 + lr) != 0.0) : (((xm[lr >> 3] >> (lr & 7)) & 1u) != 0u);
+    };
+    // dense next column: own rows; else the tile's slice of its index list
+    const int nlim = dnxt ? kTileRows : Ln.cnt;
+    for (int i = gt; i < nlim; i += GT) {
+      int lr;
+      double x;
+      if (dnxt) {
+        lr = i;
+        x = __ldg(dnxt + row0 + lr);
+        if (x == 0.0) continue;
+      } else {
+        lr = static_cast<int>(list_at(lnext, Ln, P.row_idx, i) - row0);
+        x = n_ind ? 1.0 : P.vals[Ln.lo + i];
+      }
       const double ev = *e_at(sb, lr);
-      const double x = n_ind ? 1.0 : P.vals[Ln.lo + i];
       const double eb = __dmul_rn(ev, x);
       const double ec = __dmul_rn(eb, x);
       rb = __dadd_rn(rb, eb);
@@ -935,7 +987,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
         rub = __dadd_rn(rub, __dmul_rn(u, eb));
         ruc = __dadd_rn(ruc, __dmul_rn(u, ec));
       }
-      if (ccd_cur && ((xm[lr >> 3] >> (lr & 7)) & 1u)) {
+      if (ccd_cur && in_cur(lr)) {
         rsb = __dadd_rn(rsb, eb);
         rsc = __dadd_rn(rsc, ec);
         if constexpr (FG) {
@@ -945,9 +997,15 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       }
     }
     if (ccd_cur) {
-      for (int i = gt; i < Lc.cnt; i += GT) {
-        const int32_t r = list_at(lcur, Lc, P.row_idx, i);
-        const int lr = static_cast<int>(r - row0);
+      const int clim = dcur ? kTileRows : Lc.cnt;
+      for (int i = gt; i < clim; i += GT) {
+        int lr;
+        if (dcur) {
+          lr = i;
+          if (__ldg(dcur + row0 + lr) == 0.0) continue;
+        } else {
+          lr = static_cast<int>(list_at(lcur, Lc, P.row_idx, i) - row0);
+        }
         const double ev = *e_at(sb, lr);
         rsa = __dadd_rn(rsa, ev);
         if constexpr (FG) {
@@ -1700,6 +1758,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     const long long nc =
         (kk + 1 < P.nslots) ? P.slot_col[kk + 1] : (P.mode == kModeCcd ? P.slot_col[0] : -1);
     f.col = c;
+    f.ncol = nc;
     f.kind = c >= 0 ? kSlotGrad : kSlotLoglik;
     f.cind = c >= 0 ? ((!P.has_vals || P.col_ind[c]) ? 1 : 0) : 1;
     f.nind = nc >= 0 ? ((!P.has_vals || P.col_ind[nc]) ? 1 : 0) : 1;
@@ -1710,6 +1769,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   auto set_slot_fields = [&](const SlotFields& f) {
     if (!f.valid) return;
     ss.col = f.col;
+    ss.ncol = f.ncol;
     ss.kind = f.kind;
     ss.cind = f.cind;
     ss.nind = f.nind;

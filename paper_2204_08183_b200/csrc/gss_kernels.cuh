@@ -75,6 +75,8 @@ struct CycleParams {
   const double* csr_val;       // CSR values (NULL => all 1.0)
   const double* colmax;        // [p] max |x| per column
   const uint8_t* tile_first;   // [ntiles] 1 if a stratum starts at the tile's first row
+  const int32_t* dense_idx;    // [p] dense-pool slot of a column with density >= 25%, else -1
+  const double* dense_pool;    // [ndense][npad] dense column values by device position
   // ---- engine state ----
   double* eta;                 // [npad]
   double* e;                   // [npad] exp(eta) cache (0 for masked/pad rows)
@@ -158,6 +160,10 @@ cudaError_t launch_remap_rows(int32_t* row_idx, int64_t nnz, const int64_t* dev_
                               cudaStream_t s);
 cudaError_t launch_build_tile_ptr(const int64_t* col_ptr, const int32_t* row_idx, int64_t p,
                                   int ntiles, uint32_t* tile_ptr, cudaStream_t s);
+// dense pool: pool[slot[j]][row_idx[k]] = vals[k] (or 1.0) for dense columns
+cudaError_t launch_fill_dense(const int64_t* col_ptr, const int32_t* row_idx, const double* vals,
+                              const int32_t* slot, int64_t p, int64_t npad, double* pool,
+                              cudaStream_t s);
 cudaError_t launch_colmax(const int64_t* col_ptr, const double* vals, int64_t p,
                           double* colmax, cudaStream_t s);
 cudaError_t launch_csr_count(const int32_t* row_idx, int64_t nnz, int64_t* row_cnt,

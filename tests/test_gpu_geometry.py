@@ -113,11 +113,12 @@ def test_many_tiles_per_cta_vs_oracle(capi, model, n, p, quant, strata, valued, 
 @pytest.mark.parametrize("model", ["cox", "finegray"])
 @pytest.mark.parametrize("grid", [2, 0])
 def test_dense_columns_list_fallback(capi, model, grid):
-    """Columns denser than 12.5% overflow the 256-entry shared-memory list of
-    a 2048-row tile slice; the consumers then read the slice from global
-    memory.  A 60% valued column (stored dense by the reference,
-    dataset.cpp:151-155) and a 30% all-ones column (dense, hence valued:
-    not an indicator) next to sparse indicator columns."""
+    """Dense storage (density >= 25%, SparseColumn::make dataset.cpp:126-157):
+    the 60%, 30% (all ones, hence valued) and 90% columns are read row-wise
+    from the device dense pool by the scan, the pending update and the
+    next-slot records.  The 20% column stays sparse but overflows the
+    256-entry shared-memory list of a 2048-row tile slice, so the consumers
+    read its slice from global memory.  Sparse indicator columns between."""
     rng = np.random.default_rng(99 + grid)
     n, p = 120_000, 6
     rows, cols, vals = [], [], []
