@@ -245,6 +245,35 @@ int gss_shard_sums(gss_engine* e, int64_t column, const double* carry8, double* 
 /* validate-before-mutate of update_xbeta_sparse (src/engine.cpp:171-190) without mutating */
 int gss_engine_update_validate(gss_engine* e, int64_t column, double delta, int32_t* overflow);
 
+/*
+ * In-kernel patient sharding (config C5): a communicator gives
+ * every shard engine peer-visible exchange buffers; each grid exchange of a
+ * shard's cycle kernel is then followed by one exchange of the shard
+ * aggregates (slot partials, segmented scan tails/heads, aux flags) over
+ * NVLink peer memory, combined in rank order, so every shard computes the
+ * identical Engine::finish + coordinate_step.  Cox only (Fine-Gray needs the
+ * global censoring KM).  The host CCD loop is gss_engine_fit (one process per
+ * GPU; every rank calls it) or gss_sharded_fit_local (all shards in this
+ * process, one batched launch per cycle).
+ *   gss_comm_unique_id  rank 0 creates the NCCL unique id (128 bytes); the
+ *                       caller broadcasts it (e.g. torch.distributed)
+ *   gss_comm_init       NCCL bootstrap + CUDA IPC exchange buffers
+ *   gss_comm_local      a communicator per shard engine of this process
+ *                       (attaches them and makes the fixed terms global)
+ *   gss_engine_attach_comm  engine becomes shard `rank`; fixed terms become
+ *                       the rank-ordered sums over shards (NCCL all-gather)
+ */
+typedef struct gss_comm gss_comm;
+int gss_comm_unique_id(unsigned char* out128);
+int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device, gss_comm** out);
+int gss_comm_local(gss_engine* const* shards, int count, gss_comm** comms_out);
+int gss_comm_rank(const gss_comm* c, int* nranks, int* rank);
+int gss_engine_attach_comm(gss_engine* e, gss_comm* c);
+void gss_comm_destroy(gss_comm* c);
+int gss_sharded_fit_local(gss_engine* const* shards, int count, const gss_penalty_spec* pen,
+                          const gss_fit_config* cfg, double* beta_out, gss_fit_result* res,
+                          double* device_seconds);
+
 /* Device time (ms) of the last fit's coordinate cycles, for bench. */
 int gss_engine_last_timing(gss_engine* e, double* scan_ms, int64_t* launches);
 /* Per-cycle statistics of the last fit: CUDA-event device time of each

@@ -79,7 +79,7 @@ def lib():
         L.gss_last_error.restype = ctypes.c_char_p
         L.gss_version.restype = ctypes.c_char_p
         L.gss_dataset_device_bytes.restype = ctypes.c_int64
-        for name in ("gss_dataset_release", "gss_engine_destroy"):
+        for name in ("gss_dataset_release", "gss_engine_destroy", "gss_comm_destroy"):
             getattr(L, name).restype = None
         _lib = L
     return _lib
@@ -196,6 +196,12 @@ class Engine:
         if getattr(self, "h", None) and _lib is not None:
             _lib.gss_engine_destroy(self.h)
             self.h = None
+
+    def attach_comm(self, comm):
+        """gss_engine_attach_comm: this engine becomes shard `comm.rank`."""
+        check(lib().gss_engine_attach_comm(self.h, comm.h))
+        self._comm = comm
+        return self
 
     def set_grid(self, grid):
         """CTAs per launch (0 = one per SM); re-partitions the tile ranges."""
@@ -323,6 +329,72 @@ class Engine:
         L.gss_engine_cycle_stats.restype = ctypes.c_int64
         k = L.gss_engine_cycle_stats(self.h, _p(ms), _p(acc), ctypes.c_int64(max_cycles))
         return ms[:k].copy(), acc[:k].copy()
+
+
+class Comm:
+    """gss_comm: one shard's handle on the in-kernel cross-shard exchange
+    (config C5).  Keep it alive while its engine fits."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gss_comm_destroy(self.h)
+            self.h = None
+
+    @property
+    def rank(self):
+        n, r = ctypes.c_int(), ctypes.c_int()
+        check(lib().gss_comm_rank(self.h, ctypes.byref(n), ctypes.byref(r)))
+        return r.value, n.value
+
+
+def comm_unique_id() -> bytes:
+    """gss_comm_unique_id: the NCCL bootstrap id (rank 0; broadcast it)."""
+    buf = (ctypes.c_ubyte * 128)()
+    check(lib().gss_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(nranks: int, rank: int, uid: bytes, device: int = 0) -> Comm:
+    """gss_comm_init: one process per GPU (NCCL bootstrap + CUDA IPC buffers)."""
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid[:128])
+    h = ctypes.c_void_p()
+    check(lib().gss_comm_init(int(nranks), int(rank), buf, int(device), ctypes.byref(h)))
+    return Comm(h)
+
+
+def comm_local(engines):
+    """gss_comm_local: every shard engine of this process gets a communicator
+    (rank = position) and the global fixed terms."""
+    k = len(engines)
+    hs = (ctypes.c_void_p * k)(*[e.h.value for e in engines])
+    out = (ctypes.c_void_p * k)()
+    check(lib().gss_comm_local(hs, int(k), out))
+    comms = [Comm(ctypes.c_void_p(out[i])) for i in range(k)]
+    for e, c in zip(engines, comms):
+        e._comm = c
+    return comms
+
+
+def sharded_fit_local(engines, penalty="l1", strength=0.0, tol=1e-6, max_cycles=1000,
+                      trust_init=1.0):
+    """gss_sharded_fit_local: one CCD fit over the patient shards of this
+    process (all shards in one batched launch per cycle)."""
+    k = len(engines)
+    kind = {"none": 0, "l1": 1, "l2": 2}[penalty]
+    pen = PenaltySpec(kind, float(strength), None)
+    cfg = FitConfig(tol, max_cycles, trust_init)
+    hs = (ctypes.c_void_p * k)(*[e.h.value for e in engines])
+    beta = np.zeros(engines[0].ds.p)
+    res = FitResult()
+    dev_s = ctypes.c_double()
+    check(lib().gss_sharded_fit_local(hs, int(k), ctypes.byref(pen), ctypes.byref(cfg), _p(beta),
+                                      ctypes.byref(res), ctypes.byref(dev_s)))
+    return {"beta": beta, "objective": res.objective, "cycles": res.cycles,
+            "converged": bool(res.converged), "nonzero_count": res.nonzero_count,
+            "skipped_steps": res.skipped_steps, "device_seconds": dev_s.value}
 
 
 def fit_batch(engines, penalty="l1", strengths=None, tol=1e-6, max_cycles=1000, trust_init=1.0,

@@ -33,6 +33,10 @@
 
 namespace gss {
 int set_last_error(int code, const std::string& msg);
+int engine_fixed_terms(gss_engine* e, double** dev_fixed, int64_t* p, int* device,
+                       cudaStream_t* stream);
+int engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* pay_ptrs,
+                       unsigned int* const* bar_ptrs);
 }
 using namespace gss;
 
@@ -200,6 +204,7 @@ struct gss_engine {
     gss_fit_result res{};
     double prev = 0.0;
     bool converged = false, done = false;
+    bool need_init_obj = false;  // sharded (nranks > 1): objective at beta = 0 still to come
     int64_t cycle = 0;
     int err = GSS_OK;
     std::chrono::steady_clock::time_point t0;
@@ -373,6 +378,9 @@ int run_slots(gss_engine* E, const std::vector<int32_t>& slots, int mode, bool w
   P.slot_col = E->slot_col;
   P.nslots = static_cast<int>(slots.size());
   P.mode = mode;
+  // API calls on a shard of an in-kernel sharded fit are shard-local (the
+  // cross-shard exchange runs in CCD launches, which every shard makes)
+  if (mode != kModeCcd) P.nranks = 0;
   P.slot_out = want_out ? E->slot_out : nullptr;
   P.ext = ext ? E->ext : nullptr;
   P.shard_out = prologue ? E->shard : nullptr;
@@ -1048,6 +1056,35 @@ int gss_engine_get_ipcw(gss_engine* E, double* u, double* g, int64_t n) {
   return GSS_OK;
 }
 
+int gss_sharded_fit_local(gss_engine* const* shards, int count, const gss_penalty_spec* pen,
+                          const gss_fit_config* cfg, double* beta_out, gss_fit_result* res,
+                          double* device_seconds) {
+  Nvtx nvtx_("gss_sharded_fit_local");
+  if (!shards || count < 1 || !pen || !cfg || !res) return fail(GSS_ERR_DOMAIN, "null argument");
+  for (int r = 0; r < count; ++r) {
+    if (!shards[r] || shards[r]->prm.nranks != count || shards[r]->prm.rank != r)
+      return fail(GSS_ERR_DOMAIN, "gss_sharded_fit_local: shard r must carry rank r of a local comm");
+    if (shards[r]->ds->device != shards[0]->ds->device)
+      return fail(GSS_ERR_DOMAIN, "gss_sharded_fit_local: shards must share one device "
+                                  "(one process per GPU uses gss_engine_fit)");
+  }
+  if (count > kMaxBatch || count > shards[0]->max_grid)
+    return fail(GSS_ERR_DOMAIN, "gss_sharded_fit_local: too many shards for one launch");
+  // all shards in ONE batched launch per cycle (their kernels wait on each
+  // other's exchange rows, so they must be co-resident)
+  std::vector<gss_penalty_spec> pens(static_cast<size_t>(count), *pen);
+  std::vector<gss_fit_result> rs(static_cast<size_t>(count));
+  std::vector<int32_t> st(static_cast<size_t>(count));
+  const int64_t p = shards[0]->ds->p;
+  std::vector<double> betas(static_cast<size_t>(count * p));
+  const int rc = gss_fit_batch(shards, count, pens.data(), cfg, count, betas.data(), rs.data(),
+                               st.data(), device_seconds);
+  if (rc) return rc;
+  *res = rs[0];
+  if (beta_out) std::copy(betas.begin(), betas.begin() + p, beta_out);
+  return GSS_OK;
+}
+
 int gss_engine_counters(gss_engine* E, int64_t* accepted, int64_t* refreshes) {
   int rc = check_engine(E);
   if (rc) return rc;
@@ -1115,11 +1152,18 @@ int fit_begin(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_config* 
   E->h_ctl->err_col = -1;
   rc = push_ctl(E);
   if (rc) return rc;
-  double ll = 0.0;
-  rc = gss_engine_log_likelihood(E, &ll);
-  if (rc) return rc;
-  F.prev = ll - penalty_value(&F.pen, E->h_beta);
-  F.trace[0] = F.prev;
+  if (E->prm.nranks > 1) {
+    // patient shard: the objective at beta = 0 needs every shard's carries;
+    // it is a CCD launch of the objective slot alone, made by all shards
+    // together (init_objective) before the first cycle
+    F.need_init_obj = true;
+  } else {
+    double ll = 0.0;
+    rc = gss_engine_log_likelihood(E, &ll);
+    if (rc) return rc;
+    F.prev = ll - penalty_value(&F.pen, E->h_beta);
+    F.trace[0] = F.prev;
+  }
   F.converged = p == 0;
   F.done = F.converged;
   E->cycle_ms.clear();
@@ -1150,6 +1194,33 @@ CycleParams cycle_params(const gss_engine* E) {
 }
 
 // after a cycle launch of E completed (stream synchronised by the caller)
+// The objective at beta = 0 of sharded engines (need_init_obj): one launch of
+// the objective slot in CCD mode (the cross-shard exchange runs), for all the
+// given shards together (a batched launch: they must be co-resident).
+int init_objective(gss_engine* const* es, int count) {
+  std::vector<CycleParams> prm(static_cast<size_t>(count));
+  std::vector<BatchEntry> ent(static_cast<size_t>(count));
+  for (int a = 0; a < count; ++a) {
+    gss_engine* E = es[a];
+    prm[a] = cycle_params(E);
+    prm[a].slot_col = E->slot_col + E->ds->p;  // the cycle's last slot: -1 (objective)
+    prm[a].nslots = 1;
+    ent[a] = BatchEntry{&E->tm_e, &E->tm_code, &E->tm_g, &prm[a]};
+  }
+  GSS_CUDA(count == 1 ? launch_cycle(ent[0].tm_e, ent[0].tm_code, ent[0].tm_g, prm[0], es[0]->stream)
+                      : launch_cycle_batch(ent.data(), count, es[0]->stream));
+  GSS_CUDA(cudaStreamSynchronize(es[0]->stream));
+  for (int a = 0; a < count; ++a) {
+    gss_engine* E = es[a];
+    if (int rc = sync_ctl(E)) return rc;
+    if (E->h_ctl->err_code) return device_error(E, "fit");
+    E->fs.prev = E->h_ctl->loglik - penalty_value(&E->fs.pen, E->h_beta);
+    E->fs.trace[0] = E->fs.prev;
+    E->fs.need_init_obj = false;
+  }
+  return GSS_OK;
+}
+
 int fit_after_cycle(gss_engine* E, double ms) {
   auto& F = E->fs;
   const int64_t p = E->ds->p;
@@ -1205,6 +1276,10 @@ int gss_engine_fit(gss_engine* E, const gss_penalty_spec* pen, const gss_fit_con
   *res = gss_fit_result{};
   int rc = fit_begin(E, pen, cfg);
   if (rc) return rc;
+  if (E->fs.need_init_obj) {  // one process per GPU: every rank makes this launch
+    rc = init_objective(&E, 1);
+    if (rc) return rc;
+  }
   cudaStream_t s = E->stream;
   while (!E->fs.done) {
     Nvtx nvtx_cycle("ccd cycle %lld", static_cast<long long>(E->fs.cycle + 1));
@@ -1297,6 +1372,15 @@ int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_s
     cudaEvent_t e0 = engines[queue[0]]->ev0, e1 = engines[queue[0]]->ev1;
     std::vector<CycleParams> prm;
     std::vector<BatchEntry> ent;
+    {  // sharded engines (gss_sharded_fit_local): objective at beta = 0, together
+      std::vector<gss_engine*> need;
+      for (int64_t i : active)
+        if (engines[i]->fs.need_init_obj) need.push_back(engines[i]);
+      if (!need.empty()) {
+        const int rc = init_objective(need.data(), static_cast<int>(need.size()));
+        if (rc) return rc;
+      }
+    }
     while (!active.empty()) {
       Nvtx nvtx_cycle("batched ccd cycle (%lld fits)", static_cast<long long>(active.size()));
       prm.resize(active.size());
@@ -1447,3 +1531,32 @@ int64_t gss_engine_cycle_stats(gss_engine* E, double* ms, int64_t* accepted, int
 }
 
 }  // extern "C"
+
+// ---- gss_comm.cu support -------------------------------------------------
+int gss::engine_fixed_terms(gss_engine* e, double** dev_fixed, int64_t* p, int* device,
+                            cudaStream_t* stream) {
+  if (!e) return fail(GSS_ERR_DOMAIN, "null engine handle");
+  *dev_fixed = e->fixed;
+  *p = e->ds->p;
+  *device = e->ds->device;
+  *stream = e->stream;
+  return GSS_OK;
+}
+
+int gss::engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* pay_ptrs,
+                            unsigned int* const* bar_ptrs) {
+  if (!e) return fail(GSS_ERR_DOMAIN, "null engine handle");
+  if (e->weighted)
+    return fail(GSS_ERR_DOMAIN, "patient sharding supports the Cox model (Fine-Gray needs the "
+                                "global censoring distribution)");
+  cudaSetDevice(e->ds->device);
+  if (int rc = sync_ctl(e)) return rc;
+  e->prm.nranks = nranks;
+  e->prm.rank = rank;
+  e->prm.xr_pay = pay_ptrs;
+  e->prm.xr_bar = bar_ptrs;
+  e->h_ctl->xr_base = 0;
+  e->h_ctl->xr_count = 0;
+  e->h_ctl->rec_valid = 0;
+  return push_ctl(e);
+}

@@ -121,6 +121,7 @@ struct CcdState {
   long long accepted, refreshes, skipped, err_col;
   int err;
   unsigned bar_target;
+  unsigned long long xr_base, xr_count;  // cross-shard counter base / exchanges done
   // step inputs of the current slot, prefetched at slot start
   double in_fixed, in_beta, in_hw, in_cmax;
   int in_pen, in_ind;
@@ -185,6 +186,9 @@ struct Tail {
   uint8_t tfirst[MaxTc<FG>::v];  // tile_first of the CTA's first MaxTc tiles
   int cstar, cend;
   int ext_f, ext_r;
+  double xext[12];      // cross-shard carry: fwd (a,b,c,sa,sb,sc) of earlier shards,
+                        // rev (ua..usc) of later shards (in-kernel exchange)
+  double xaux[2];       // cross-shard aux: max |eta| (refresh), overflow flag (validation)
   volatile unsigned mark[32];  // last phase reached by each warp (watchdog report)
   CcdState cs;
   // per-tile records and in-range carries of the CTA's first kMaxTc tiles live
@@ -1576,14 +1580,22 @@ __device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl,
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     double v = __dadd_rn(tl->gs[3 + i], __dmul_rn(k1, tl->gs[6 + i]));
-    if (tl->ext_f) v = __dadd_rn(__ldcg(P.ext + i), v);  // shards before this one
+    if (tl->ext_f) {  // shards before this one
+      const double x = P.nranks > 1 ? __dadd_rn(tl->xext[i], __dmul_rn(k1, tl->xext[3 + i]))
+                                    : __ldcg(P.ext + i);
+      v = __dadd_rn(x, v);
+    }
     tl->ss.cin_f[i] = v;
   }
   if constexpr (FG) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       double v = __dadd_rn(tl->gs[9 + i], __dmul_rn(k1, tl->gs[12 + i]));
-      if (tl->ext_r) v = __dadd_rn(v, __ldcg(P.ext + 4 + i));  // shards after this one
+      if (tl->ext_r) {  // shards after this one
+        const double x = P.nranks > 1 ? __dadd_rn(tl->xext[6 + i], __dmul_rn(k1, tl->xext[9 + i]))
+                                      : __ldcg(P.ext + 4 + i);
+        v = __dadd_rn(v, x);
+      }
       tl->ss.cin_r[i] = v;
     }
   }
@@ -1665,6 +1677,119 @@ __device__ __forceinline__ void consumer_tasks(const CycleParams& P, Tail<FG>* t
 }
 
 // ---------------------------------------------------------------------------
+// Cross-shard exchange (patient-sharded fit, config C5): after a grid exchange
+// and gather, CTA 0 of every shard publishes the shard's aggregate — slot
+// partials, the segmented fwd tail from its last stratum-starting CTA (with
+// s-parts), the rev head up to its first one, aux values — to every shard's
+// buffer with peer stores, then a system-scope release arrival on every
+// shard's counter; every CTA of every shard waits for all arrivals and
+// combines the rows in RANK order: identical partial sums (hence identical
+// coordinate steps) everywhere, and the carries from the other shards
+// (src/scan_kernels.hpp:114-134 combines chunks the same way).  Lane 0.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool FG>
+__device__ void cross_shard(const CycleParams& P, Tail<FG>* tl, int cta, double aux0, double aux1) {
+  const int R = P.nranks, me = P.rank, G = P.grid;
+  CcdState& cs = tl->cs;
+  const unsigned long long xc = cs.xr_count;
+  const size_t slot = (xc & 1ull) * size_t(R);
+  if (cta == 0) {
+    double row[kXrStride];
+#pragma unroll
+    for (int i = 0; i < kXrStride; ++i) row[i] = 0.0;
+    row[0] = tl->gs[0];
+    row[1] = tl->gs[1];
+    row[2] = tl->gs[2];
+    int last = -1, first = G;
+    for (int c = 0; c < G; ++c)
+      if (tl->cflag[c]) {
+        last = c;
+        if (first == G) first = c;
+      }
+    row[3] = last >= 0 ? 1.0 : 0.0;
+    for (int c = (last < 0 ? 0 : last); c < G; ++c)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) row[4 + i] = __dadd_rn(row[4 + i], tl->gbuf[c][4 + i]);
+    if constexpr (FG) {
+      const int end = first == G ? G - 1 : first;
+      for (int c = 0; c <= end; ++c)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) row[10 + i] = __dadd_rn(row[10 + i], tl->gbuf[c][10 + i]);
+    }
+    row[16] = aux0;
+    row[17] = aux1;
+    for (int q = 0; q < R; ++q) {
+      double* dst = P.xr_pay[q] + (slot + me) * kXrStride;
+      for (int i = 0; i < 18; ++i) dst[i] = row[i];
+    }
+    // release-reduction at system scope: orders this thread's row stores
+    // before the arrival (no separate fence round trip)
+    for (int q = 0; q < R; ++q)
+      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(P.xr_bar[q]) : "memory");
+  }
+  const unsigned target = static_cast<unsigned>(cs.xr_base + (xc + 1) * static_cast<unsigned long long>(R));
+  const unsigned* mybar = P.xr_bar[me];
+  const unsigned long long t0 = gtimer();
+  unsigned it = 0;
+  while (static_cast<int>(ld_acquire_sys_u32(mybar) - target) < 0) {
+    if ((++it & 1023u) == 0 && gtimer() - t0 > 2 * kWatchdogNs)
+      watchdog_trap("cross-shard exchange", ld_acquire_sys_u32(mybar), target);
+  }
+  const double* rows = P.xr_pay[me] + slot * kXrStride;
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, a0 = 0.0, a1 = 0.0;
+  for (int q = 0; q < R; ++q) {
+    const double* r = rows + size_t(q) * kXrStride;
+    g0 = __dadd_rn(g0, __ldcv(r + 0));
+    g1 = __dadd_rn(g1, __ldcv(r + 1));
+    g2 = __dadd_rn(g2, __ldcv(r + 2));
+    a0 = fmax(a0, __ldcv(r + 16));
+    a1 = fmax(a1, __ldcv(r + 17));
+  }
+  tl->gs[0] = g0;
+  tl->gs[1] = g1;
+  tl->gs[2] = g2;
+  tl->xaux[0] = a0;
+  tl->xaux[1] = a1;
+  // fwd: tails of shards start .. me-1 (start = the last earlier shard with a
+  // stratum start); rev: heads of shards me+1 .. end (end = the first later
+  // shard with a stratum start)
+  int start = 0;
+  for (int q = me - 1; q >= 0; --q)
+    if (__ldcv(rows + size_t(q) * kXrStride + 3) != 0.0) {
+      start = q;
+      break;
+    }
+  double f[6] = {0, 0, 0, 0, 0, 0};
+  for (int q = start; q < me; ++q)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) f[i] = __dadd_rn(f[i], __ldcv(rows + size_t(q) * kXrStride + 4 + i));
+#pragma unroll
+  for (int i = 0; i < 6; ++i) tl->xext[i] = f[i];
+  if constexpr (FG) {
+    int end = R - 1;
+    for (int q = me + 1; q < R; ++q)
+      if (__ldcv(rows + size_t(q) * kXrStride + 3) != 0.0) {
+        end = q;
+        break;
+      }
+    double r6[6] = {0, 0, 0, 0, 0, 0};
+    for (int q = me + 1; q <= end; ++q)
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        r6[i] = __dadd_rn(r6[i], __ldcv(rows + size_t(q) * kXrStride + 10 + i));
+#pragma unroll
+    for (int i = 0; i < 6; ++i) tl->xext[6 + i] = r6[i];
+  }
+  cs.xr_count = xc + 1;
+}
+
+// ---------------------------------------------------------------------------
 // the control warp: per slot, the in-range carry scan of the records as the
 // consumers release tiles, then (once the slot is consumed) the partial sums,
 // the grid exchange, the fixed-order gather, Engine::finish + coordinate_step
@@ -1697,6 +1822,8 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   CcdState& cs = tl->cs;
   if (lane == 0) {
     cs.bar_target = static_cast<unsigned>(ctl->bar_base);
+    cs.xr_base = ctl->xr_base;
+    cs.xr_count = ctl->xr_count;
     cs.absmax = __longlong_as_double(static_cast<long long>(ctl->eta_absmax_bits));
     cs.slack = ctl->bound_slack;
     cs.accepted = ctl->accepted;
@@ -1739,7 +1866,15 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   int& cstar = cs.cstar;
   int& cend = cs.cend;
   // full range scan of the records + publish + exchange + gather
-  auto publish_full = [&](double p0, double p1, double pb) {
+  // cross-shard step after a gather (patient-sharded launches only): aux0 /
+  // aux1 are this shard's max |eta| / overflow flag, combined into tl->xaux
+  auto xshard = [&](double aux0, double aux1) {
+    if (P.nranks <= 1) return;
+    __syncwarp();
+    if (lane == 0) cross_shard<FG>(P, tl, cta, aux0, aux1);
+    __syncwarp();
+  };
+  auto publish_full = [&](double p0, double p1, double pb, int auxmode = 0) {
     double* pm = wbuf();
     range_scan<FG>(P, tl, t0, tc, pm, lane);
     if (lane == 0) {
@@ -1749,6 +1884,12 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     }
     exchange();
     gather_warp<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, lane);
+    double mm = 0.0;
+    if (auxmode == 1 && lane == 0 && P.nranks > 1) {  // refresh: this shard's max |eta|
+      const double* pa = raux(xi - 1);
+      for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayAux + 0));
+    }
+    xshard(mm, 0.0);
   };
   auto slot_fields = [&](int kk) {
     SlotFields f{};
@@ -1794,6 +1935,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   if (P.prologue_only) {
     if (lane == 0 && cta == 0) {
       ctl->bar_base = bar_target;
+      ctl->xr_count = cs.xr_count;
       ctl->rec_valid = err ? 0 : 1;  // the records serve the launch that follows
       ctl->rec_col = P.slot_col[0];
     }
@@ -1906,6 +2048,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       exchange();
       pmark(1);
       gather_warp<FG>(P, rbuf(xi - 1), cta, cstar, cend, tl, lane);
+      xshard(0.0, 0.0);
     }
     pmark(2);
     // ---- finish + coordinate step (lane 0, replicated in every CTA) ----
@@ -1989,10 +2132,22 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       wait_done();
       if (lane == 0) waux()[1] = tl->flag ? 1.0 : 0.0;
       exchange();
+      double anyd = 0.0;
       if (lane == 0) {
         const double* pa = raux(xi - 1);
-        bool any = false;
-        for (int c = 0; c < G; ++c) any |= __ldcg(pa + size_t(c) * kPayAux + 1) != 0.0;
+        for (int c = 0; c < G; ++c) anyd = fmax(anyd, __ldcg(pa + size_t(c) * kPayAux + 1));
+      }
+      if (P.nranks > 1) {  // OR over shards (validate-before-mutate on every shard)
+        __syncwarp();
+        if (lane == 0) {
+          tl->gs[0] = tl->gs[1] = tl->gs[2] = 0.0;
+          cross_shard<FG>(P, tl, cta, 0.0, anyd);
+          anyd = tl->xaux[1];
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        const bool any = anyd != 0.0;
         if (any) {
           if (!err) {
             err = kErrOverflow;
@@ -2039,12 +2194,13 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
         for (int w = 0; w < W; ++w) mm = fmax(mm, tl->wpart[w][3]);
         waux()[0] = mm;
       }
-      publish_full(0.0, 0.0, 0.0);
+      publish_full(0.0, 0.0, 0.0, 1);
       if (lane == 0) {
         set_carry_in<FG>(P, tl, 0.0);
         const double* pa = raux(xi - 1);
         double mm = 0.0;
         for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayAux + 0));
+        if (P.nranks > 1) mm = tl->xaux[0];  // max over shards
         absmax = mm;  // the bound is exact again
         slack = 0.0;
       }
@@ -2076,6 +2232,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   // ---- epilogue: CTA 0 persists the replicated state ----
   if (lane == 0 && cta == 0) {
     ctl->bar_base = bar_target;
+    ctl->xr_count = cs.xr_count;
     ctl->eta_absmax_bits = static_cast<unsigned long long>(__double_as_longlong(absmax));
     ctl->bound_slack = slack;
     ctl->accepted = accepted;
@@ -2172,8 +2329,9 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
     tl->cstar = cs;
     tl->cend = ce;
     // carry from other shards reaches this CTA when no stratum starts between
-    tl->ext_f = (P.ext && !fs) ? 1 : 0;
-    tl->ext_r = (P.ext && !fe) ? 1 : 0;
+    tl->ext_f = ((P.ext || P.nranks > 1) && !fs) ? 1 : 0;
+    tl->ext_r = ((P.ext || P.nranks > 1) && !fe) ? 1 : 0;
+    for (int i = 0; i < 12; ++i) tl->xext[i] = 0.0;
   }
 
   if (warp > W) {

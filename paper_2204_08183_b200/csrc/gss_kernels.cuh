@@ -24,6 +24,8 @@ struct Ctl {
   int err_code;                        // gss_status of the first error (0 = none)
   int pad1;
   long long err_col;
+  unsigned long long xr_base;          // cross-shard counter value at launch start
+  unsigned long long xr_count;         // cross-shard exchanges so far (buffer parity)
   // results of the last slot of each kind
   double grad_sum, hess_sum, gradient, hessian, fixed_term;
   double ll_fixed, ll_logden, loglik;
@@ -116,7 +118,15 @@ struct CycleParams {
                                // [0] stratum-start flag, [1..3] fwd tail, [4..6] rev head
   int prologue_only;           // stop after the prologue (records + shard aggregate)
   int reuse_records;           // API mode: records from a prologue-only launch are valid
+  // ---- in-kernel cross-shard exchange (gss_comm): every grid exchange of
+  // this shard's launch is followed by one exchange of the shard aggregates
+  // (kXrStride doubles per rank) over peer memory, so all shards run the
+  // same fixed-order reduction and the same coordinate step ----
+  int nranks, rank;            // nranks > 1 enables it
+  double* const* xr_pay;       // [nranks] rank q's buffer [2][nranks][kXrStride] (peer-mapped)
+  unsigned int* const* xr_bar; // [nranks] rank q's arrival counter (peer-mapped)
 };
+constexpr int kXrStride = 24;
 
 // Kernel parameter block of one cycle-kernel launch over K engines (fits):
 // CTAs [cta_base[f], cta_base[f+1]) run engine f with its own parameters,

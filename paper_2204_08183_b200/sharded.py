@@ -131,6 +131,10 @@ class ShardedFit:
         self.x = exchange
         self.world = exchange.world
         self.bounds = shard_bounds(ds.times, ds.stratum_start, self.world)
+        if any(self.bounds[r + 1] <= self.bounds[r] for r in range(self.world)):
+            # the same error on every rank before any collective (no rank waits)
+            raise ValueError(f"cannot cut {len(ds.times)} rows into {self.world} non-empty "
+                             f"shards at tied-block boundaries: {self.bounds}")
         self.p = len(ds.col_ptr) - 1
         self.engines, self._ds = [], []
         for r in exchange.ranks:
@@ -218,3 +222,56 @@ class ShardedFit:
                 "objective_trace": np.array(trace), "skipped_steps": skipped,
                 "monotonicity_violations": violations,
                 "nonzero_count": int(np.count_nonzero(beta)), "shards": self.bounds}
+
+
+# ---------------------------------------------------------------------------
+# In-kernel exchange (gss_comm): the shards' cycle kernels exchange their
+# aggregates over peer memory after every grid exchange, so the whole CCD fit
+# runs on the device with the C++ host loop (gss_engine_fit per rank, or
+# gss_sharded_fit_local for every shard of this process) — no host step per
+# coordinate, no collective calls on the data path.
+# ---------------------------------------------------------------------------
+def shard_engines(ds, world: int, device: int = 0, ranks=None, recompute_interval: int = 100):
+    """Engines over the contiguous row shards of `ds` (shard_bounds cuts)."""
+    bounds = shard_bounds(ds.times, ds.stratum_start, world)
+    if any(bounds[r + 1] <= bounds[r] for r in range(world)):
+        raise ValueError(f"cannot cut {len(ds.times)} rows into {world} non-empty shards at "
+                         f"tied-block boundaries: {bounds}")
+    ranks = range(world) if ranks is None else ranks
+    out = []
+    for r in ranks:
+        d = shard_dataset(ds, bounds[r], bounds[r + 1], device)
+        e = capi.Engine(d, "cox", recompute_interval)
+        e._ds_keep = d
+        out.append(e)
+    return out, bounds
+
+
+def fit_in_kernel_local(ds, world: int, device: int = 0, penalty="l1", strength=0.0, tol=1e-6,
+                        max_cycles=1000, recompute_interval: int = 100):
+    """Config C5 emulated in one process: `world` shards on one GPU, one
+    batched launch per cycle, cross-shard exchange inside the kernel."""
+    engines, bounds = shard_engines(ds, world, device, recompute_interval=recompute_interval)
+    capi.comm_local(engines)
+    r = capi.sharded_fit_local(engines, penalty, strength, tol, max_cycles)
+    r["shards"] = bounds
+    return r
+
+
+def fit_in_kernel_distributed(ds, penalty="l1", strength=0.0, tol=1e-6, max_cycles=1000,
+                              device=None, recompute_interval: int = 100):
+    """Config C5, one process per GPU (torchrun): rank r fits shard r; the NCCL
+    bootstrap id is broadcast with torch.distributed, then the exchange runs
+    over CUDA-IPC peer memory inside the kernels."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    dev = device if device is not None else __import__("torch").cuda.current_device()
+    box = [capi.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    comm = capi.comm_init(world, rank, box[0], dev)
+    (eng,), bounds = shard_engines(ds, world, dev, ranks=[rank],
+                                   recompute_interval=recompute_interval)
+    eng.attach_comm(comm)
+    r = eng.fit(penalty=penalty, strength=strength, tol=tol, max_cycles=max_cycles)
+    r["shards"] = bounds
+    return r

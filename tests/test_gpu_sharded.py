@@ -58,3 +58,55 @@ def test_shard_cuts_respect_tied_blocks(mods):
     assert cuts[0] == 0 and cuts[-1] == len(t)
     for c in cuts[1:-1]:
         assert c == len(t) or t[c] != t[c - 1]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("n,quant,strata,interval", [(60_000, 40.0, None, 100),
+                                                     (45_001, 25.0, 5, 100),
+                                                     (20_000, None, None, 7)])
+def test_in_kernel_sharded_fit_matches_oracle(mods, world, n, quant, strata, interval):
+    """The in-kernel cross-shard exchange (gss_comm_local + gss_sharded_fit_local:
+    every shard's cycle kernel publishes its aggregate to the others' peer
+    buffers after each grid exchange) reproduces the unsharded CCD fit: same
+    cycles, coefficients within 1e-8, including refreshes (interval 7) and
+    strata that span shard cuts."""
+    capi, sharded = mods
+    ds = _random_sorted(n, 8, 0.05, seed=n + 17 * world, quant=quant, strata=strata)
+    r = sharded.fit_in_kernel_local(ds, world, penalty="l1", strength=1.5, max_cycles=8,
+                                    recompute_interval=interval)
+    ref = orc.OracleEngine(ds, "cox", recompute_interval=interval).fit(
+        penalty="l1", strength=1.5, max_cycles=8)
+    assert r["cycles"] == ref["cycles"]
+    assert np.max(rel(r["beta"], ref["beta"])) < TOL_BETA
+    assert rel(r["objective"], ref["objective"]) < TOL_DERIV
+    one = capi.Engine(capi.Dataset.from_sorted(ds), "cox", interval).fit(
+        penalty="l1", strength=1.5, max_cycles=8)
+    assert one["cycles"] == r["cycles"]
+    assert np.max(rel(r["beta"], one["beta"])) < TOL_BETA
+
+
+def test_in_kernel_shards_refuse_finegray_and_empty_cuts(mods):
+    capi, sharded = mods
+    ds = _random_sorted(5_000, 3, 0.05, seed=3, quant=2.0)
+    with pytest.raises(ValueError):
+        sharded.shard_engines(ds, 4000)
+    d = capi.Dataset.from_sorted(ds)
+    e = capi.Engine(d, "cox")
+    assert capi.lib().gss_engine_attach_comm(e.h, None) != 0  # null comm -> error, no crash
+
+
+def test_comm_init_single_rank_bootstrap(mods):
+    """The multi-process path's bootstrap (NCCL unique id -> ncclCommInitRank
+    -> CUDA IPC export/all-gather of the exchange buffers) on one rank; a
+    one-rank communicator leaves the fit unchanged (no cross exchange)."""
+    capi, sharded = mods
+    ds = _random_sorted(20_000, 5, 0.05, seed=5, quant=30.0)
+    uid = capi.comm_unique_id()
+    assert len(uid) == 128
+    comm = capi.comm_init(1, 0, uid, 0)
+    assert comm.rank == (0, 1)
+    d = capi.Dataset.from_sorted(ds)
+    a = capi.Engine(d, "cox").attach_comm(comm).fit(penalty="l1", strength=1.0, max_cycles=5)
+    b = capi.Engine(d, "cox").fit(penalty="l1", strength=1.0, max_cycles=5)
+    assert a["cycles"] == b["cycles"]
+    np.testing.assert_array_equal(a["beta"], b["beta"])
