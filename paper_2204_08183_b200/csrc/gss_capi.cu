@@ -412,16 +412,18 @@ int partition_ctas(gss_engine* E, int grid) {
   grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
   std::vector<double> w(static_cast<size_t>(nt), 1.0);
   static const double kPassW =
-      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.1;
+  static const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
   for (int t = 0; t < nt; ++t) {
-    int work = 0;
+    int work = 0, ends = 0;
     for (int pass = 0; pass < kTileRows / 256; ++pass) {
-      bool any = false;
-      for (int r = 0; r < 256 && !any; ++r)
-        any = (E->h_code[size_t(t) * kTileRows + pass * 256 + r] & kCodeCount) != 0;
+      int any = 0;
+      for (int r = 0; r < 256; ++r)
+        any += (E->h_code[size_t(t) * kTileRows + pass * 256 + r] & kCodeCount) != 0;
       work += any ? 1 : 0;
+      ends += any;
     }
-    w[t] = 1.0 + kPassW * work;
+    w[t] = 1.0 + kPassW * work + kBeW * double(ends) / kTileRows;
   }
   double tot = 0.0;
   for (double x : w) tot += x;

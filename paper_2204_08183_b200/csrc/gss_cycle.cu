@@ -122,6 +122,7 @@ struct CcdState {
   int err;
   unsigned bar_target;
   unsigned long long xr_base, xr_count;  // cross-shard counter base / exchanges done
+  unsigned long long tgo, tcons;         // GSS_DEBUG & 65536: per-CTA consume time
   // step inputs of the current slot, prefetched at slot start
   double in_fixed, in_beta, in_hw, in_cmax;
   int in_pen, in_ind;
@@ -1833,6 +1834,8 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     cs.err_col = ctl->err_col;
     cs.xi = 0;
     cs.qbase = 0;
+    cs.tgo = 0;
+    cs.tcons = 0;
     // accepted updates until the next refresh (accepted % interval == 0)
     cs.to_refresh = P.recompute_interval - (cs.accepted % P.recompute_interval);
   }
@@ -2021,10 +2024,12 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       }
     }
     wait_done();  // slot consumed: partials in wpart
+    if ((P.dbg & 65536) && lane == 0 && k > 0) cs.tcons += gtimer() - cs.tgo;
     pmark(0);
     if (lane == 0) qbase += static_cast<unsigned>(tc);
     __syncwarp();
     if (P.dbg & 16) {  // ablation: stream only
+      if ((P.dbg & 65536) && lane == 0) cs.tgo = gtimer();
       go(kTaskNext);
       continue;
     }
@@ -2226,8 +2231,12 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       set_slot_fields(nf);
     }
     pmark(3);
+    if ((P.dbg & 65536) && lane == 0) cs.tgo = gtimer();
     go(kTaskNext);
   }
+  if ((P.dbg & 65536) && lane == 0)
+    printf("gss cta %d tiles %d [%d, %d) consume_us %.2f\n", cta, tc, t0, t0 + tc,
+           P.nslots > 1 ? double(cs.tcons) / (P.nslots - 1) / 1000.0 : 0.0);
 
   // ---- epilogue: CTA 0 persists the replicated state ----
   if (lane == 0 && cta == 0) {
