@@ -412,7 +412,7 @@ int partition_ctas(gss_engine* E, int grid) {
   grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
   std::vector<double> w(static_cast<size_t>(nt), 1.0);
   static const double kPassW =
-      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.1;
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
   static const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
   for (int t = 0; t < nt; ++t) {
     int work = 0, ends = 0;
