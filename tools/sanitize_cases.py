@@ -64,6 +64,38 @@ def main():
         print("exact-path fit cycles", r["cycles"])
     except capi.GssError as exc:
         print("exact-path fit raised", exc.kind)
+    # round 2 paths: dense-column pool (60% density), batched multi-fit,
+    # in-kernel cross-shard exchange (2 local shards), device ingestion
+    rng = np.random.default_rng(3)
+    rows, cols, vals = [], [], []
+    for j, dens in enumerate([0.6, 0.05, 0.3]):
+        r = np.sort(rng.choice(n, size=int(dens * n), replace=False))
+        rows.append(r)
+        cols.append(np.full(r.size, j))
+        vals.append(np.round(rng.normal(size=r.size), 2) + 0.01)
+    t = np.ceil(rng.exponential(size=n) * 20) / 20
+    st = (rng.random(n) < 0.7).astype(np.int64)
+    dsd = orc.assemble(t, st, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), 3)
+    for model in ("cox", "finegray"):
+        e = capi.Engine(capi.Dataset.from_sorted(dsd), model, recompute_interval=3).set_grid(grid)
+        e.load_beta(np.array([0.1, -0.1, 0.05]))
+        for j in range(3):
+            e.grad_hessian(j)
+        print("dense", model, "cycles", e.fit(penalty="l1", strength=0.5, max_cycles=3)["cycles"],
+              flush=True)
+    ds = data(n, 5, 11)
+    dd = capi.Dataset.from_sorted(ds)
+    res, _ = capi.fit_batch([capi.Engine(dd, "cox"), capi.Engine(dd, "cox")], "l1", [0.5, 1.0],
+                            max_cycles=3)
+    print("batched fits", [r["cycles"] for r in res], flush=True)
+    from paper_2204_08183_b200 import sharded
+    r = sharded.fit_in_kernel_local(data(2 * n, 5, 13), 2, penalty="l1", strength=0.5,
+                                    max_cycles=3, recompute_interval=4)
+    print("sharded in-kernel fit cycles", r["cycles"], flush=True)
+    import survscan
+    dsx = survscan.dataset_from_coo(t, st, np.concatenate(rows), np.concatenate(cols),
+                                    np.concatenate(vals), 3, rng.integers(0, 4, n))
+    print("device ingestion nnz", dsx.nnz_total, flush=True)
     print("sanitize cases done")
 
 
