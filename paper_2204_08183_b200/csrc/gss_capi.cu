@@ -1551,6 +1551,7 @@ int gss::engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* 
   if (e->weighted)
     return fail(GSS_ERR_DOMAIN, "patient sharding supports the Cox model (Fine-Gray needs the "
                                 "global censoring distribution)");
+  if (nranks > 16) return fail(GSS_ERR_DOMAIN, "patient sharding supports at most 16 shards");
   cudaSetDevice(e->ds->device);
   if (int rc = sync_ctl(e)) return rc;
   e->prm.nranks = nranks;
