@@ -324,6 +324,49 @@ def parity_spot_check(sim, eng, cols=(0, 1777, 4999)):
             "checker_seconds": round(time.perf_counter() - t0, 2)}
 
 
+def run_c2_fit_parity(args, dist):
+    """North-star target at C2 scale: a full L1 fit (tol 1e-6) at N = 10M rows
+    converges to the REFERENCE's coefficients.  Same COO data (the CPU-sample
+    generator, 20 columns so the reference finishes in seconds on the host
+    cores) through the drop-in survscan API (device ingestion + cycle kernel)
+    and through the unmodified reference; equal cycle counts, coefficients
+    within 1e-8 (north star)."""
+    import survscan
+    ps = args.cpu_sample_p
+    t, s, rows, cols = cpu_sample(args.n, ps, args.density, args.seed + 5, args.quantum,
+                                  args.censoring_quantile)
+    vals = np.ones(len(rows))
+    gds = survscan.dataset_from_coo(t, s, rows, cols, vals, ps)
+    t0 = time.perf_counter()
+    g = survscan.fit(gds, model="cox", penalty="l1", strength=args.strength, tol=1e-6,
+                     max_cycles=200, device=dist.local)
+    gpu_s = time.perf_counter() - t0
+    out = {"workload": f"C2-scale fit: N={args.n}, p={ps}, density {args.density}, Breslow ties "
+                       f"(q=1e-3), cq={args.censoring_quantile}, L1 gamma=sqrt(2), tol 1e-6",
+           "gpu_cycles": int(g["cycles"]), "gpu_seconds": round(gpu_s, 3),
+           "gpu_objective": g["objective"]}
+    try:
+        ref = reference_module()
+        threads = len(os.sched_getaffinity(0))
+        rds = ref.dataset_from_coo(t, s, rows, cols, vals, ps)
+        t0 = time.perf_counter()
+        r = ref.fit(rds, model="cox", penalty="l1", strength=args.strength, tol=1e-6,
+                    max_cycles=200, threads=threads, chunk_size=max(4096, -(-args.n // threads)))
+        ref_s = time.perf_counter() - t0
+        gb, rb = np.asarray(g["beta"]), np.asarray(r["beta"])
+        err = float(np.max(np.abs(gb - rb) / np.maximum(1.0, np.abs(rb))))
+        out.update({"reference_cycles": int(r["cycles"]), "reference_seconds": round(ref_s, 3),
+                    "reference_cores": threads, "reference_objective": r["objective"],
+                    "max_rel_err_beta": err,
+                    "rel_err_objective": abs(g["objective"] - r["objective"]) /
+                    max(1.0, abs(r["objective"])),
+                    "tolerance_beta": 1e-8,
+                    "pass": bool(err < 1e-8 and int(r["cycles"]) == int(g["cycles"]))})
+    except Exception as exc:  # pragma: no cover - reference module missing on the box
+        out["reference_unavailable"] = str(exc)[:200]
+    return out
+
+
 def run_c1(dist):
     """Config C1 (BASELINE configs[0]) on the reference's own data
     (tests/golden/c1_ref.npz, produced by the reference's simulate_cox seed 1):
@@ -434,6 +477,7 @@ def run_gss(args, dist):
         except Exception as exc:  # pragma: no cover - reported, never hides the main line
             c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     c1 = run_c1(dist) if (dist.rank == 0 and not args.no_c1) else None
+    c2fit = run_c2_fit_parity(args, dist) if (dist.rank == 0 and not args.no_parity) else None
     out = {
         "metric": "cox_ccd_coordinate_updates_per_s",
         "value": round(value, 2),
@@ -475,6 +519,8 @@ def run_gss(args, dist):
         out["secondary"]["c3_finegray"] = c3
     if c1 is not None:
         out["secondary"]["c1_time_to_fit"] = c1
+    if c2fit is not None:
+        out["secondary"]["c2_fit_vs_reference"] = c2fit
     if c4 is not None:
         out["secondary"]["c4_cv"] = c4
     if c5 is not None:
