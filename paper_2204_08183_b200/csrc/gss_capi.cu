@@ -36,7 +36,7 @@ int set_last_error(int code, const std::string& msg);
 int engine_fixed_terms(gss_engine* e, double** dev_fixed, int64_t* p, int* device,
                        cudaStream_t* stream);
 int engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* pay_ptrs,
-                       unsigned int* const* bar_ptrs);
+                       unsigned int* const* bar_ptrs, int sys_scope);
 }
 using namespace gss;
 
@@ -1546,7 +1546,7 @@ int gss::engine_fixed_terms(gss_engine* e, double** dev_fixed, int64_t* p, int* 
 }
 
 int gss::engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* pay_ptrs,
-                            unsigned int* const* bar_ptrs) {
+                            unsigned int* const* bar_ptrs, int sys_scope) {
   if (!e) return fail(GSS_ERR_DOMAIN, "null engine handle");
   if (e->weighted)
     return fail(GSS_ERR_DOMAIN, "patient sharding supports the Cox model (Fine-Gray needs the "
@@ -1556,6 +1556,7 @@ int gss::engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* 
   if (int rc = sync_ctl(e)) return rc;
   e->prm.nranks = nranks;
   e->prm.rank = rank;
+  e->prm.xr_sys = sys_scope;
   e->prm.xr_pay = pay_ptrs;
   e->prm.xr_bar = bar_ptrs;
   e->h_ctl->xr_base = 0;

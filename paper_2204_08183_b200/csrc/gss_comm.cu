@@ -29,7 +29,7 @@
 namespace gss {
 int set_last_error(int code, const std::string& msg);                       // gss_capi.cu
 int engine_attach_comm(gss_engine* e, int nranks, int rank, double* const* pay_ptrs,
-                       unsigned int* const* bar_ptrs);                      // gss_capi.cu
+                       unsigned int* const* bar_ptrs, int sys_scope);       // gss_capi.cu
 int engine_fixed_terms(gss_engine* e, double** dev_fixed, int64_t* p, int* device,
                        cudaStream_t* stream);                               // gss_capi.cu
 }  // namespace gss
@@ -44,7 +44,7 @@ struct gss_comm {
   unsigned int** d_bar = nullptr;    // device array [nranks] of peer-mapped counters
   std::vector<void*> opened;         // IPC-opened peer allocations
   void* nccl = nullptr;              // ncclComm_t (multi-process)
-  bool shares_arrays = false;        // d_pay / d_bar owned by another comm (local group)
+  bool sys_scope = true;             // ranks on several devices (false: one device)
 };
 
 namespace {
@@ -219,8 +219,11 @@ int gss_comm_local(gss_engine* const* shards, int count, gss_comm** comms_out) {
           return bail(set_last_error(GSS_ERR_CUDA, "gss_comm_local: no peer access between devices"));
         cudaGetLastError();
       }
+  bool one_device = true;
+  for (int r = 1; r < count; ++r) one_device &= devs[r] == devs[0];
   for (int r = 0; r < count; ++r) {
     cudaSetDevice(devs[r]);
+    cs[r]->sys_scope = !one_device;
     if (int rc = upload_ptrs(cs[r], pay, bar)) return bail(rc);
   }
   for (int r = 0; r < count; ++r)
@@ -275,7 +278,7 @@ int gss_engine_attach_comm(gss_engine* e, gss_comm* c) {
       for (int64_t j = 0; j < p; ++j) sum[j] += h[size_t(q) * p + j];
     cudaMemcpy(fx, sum.data(), sum.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
-  return gss::engine_attach_comm(e, c->nranks, c->rank, c->d_pay, c->d_bar);
+  return gss::engine_attach_comm(e, c->nranks, c->rank, c->d_pay, c->d_bar, c->sys_scope ? 1 : 0);
 }
 
 int gss_comm_local_finalize(gss_engine* const* shards, int count) {

@@ -123,6 +123,7 @@ struct CycleParams {
   // (kXrStride doubles per rank) over peer memory, so all shards run the
   // same fixed-order reduction and the same coordinate step ----
   int nranks, rank;            // nranks > 1 enables it
+  int xr_sys;                  // shards on several devices: system-scope release/acquire
   double* const* xr_pay;       // [nranks] rank q's buffer [2][nranks][kXrStride] (peer-mapped)
   unsigned int* const* xr_bar; // [nranks] rank q's arrival counter (peer-mapped)
 };
