@@ -197,11 +197,6 @@ struct Tail {
   // from / flushed to global at launch start / end
   alignas(128) double gbuf[kMaxGrid][kPayStride];  // staged CTA payloads (gather)
   uint64_t gbar;                                    // gather bulk-copy barrier
-  uint64_t xmbar;                                   // cross-shard rows bulk-copy barrier
-  uint32_t xphase;
-  double* xpay[16];                                 // cross-shard buffers (pointer table copy)
-  unsigned int* xbar[16];
-  alignas(16) double xrows[16][24];                 // one exchange's shard rows (kXrStride)
   uint32_t gphase;
   double gred[32][FG ? 15 : 9];                      // gather cross-lane partials
   double srec[MaxTc<FG>::v][FG ? 12 : 6];
@@ -1700,128 +1695,104 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
 }
 
 template <bool FG>
-__device__ void cross_shard(const CycleParams& P, Tail<FG>* tl, int cta, int lane, double aux0,
-                            double aux1) {
+__device__ void cross_shard(const CycleParams& P, Tail<FG>* tl, int cta, double aux0, double aux1) {
   const int R = P.nranks, me = P.rank, G = P.grid;
   CcdState& cs = tl->cs;
   const unsigned long long xc = cs.xr_count;
   const size_t slot = (xc & 1ull) * size_t(R);
   if (cta == 0) {
-    // this shard's row, warp-parallel: lanes sum strided CTAs of the fwd
-    // tail (from the last stratum-starting CTA) and rev head (up to the
-    // first), a fixed shuffle tree folds them; lanes 0..17 store the row into
-    // every shard's buffer (peer stores), lane 0 arrives
+    double row[kXrStride];
+#pragma unroll
+    for (int i = 0; i < kXrStride; ++i) row[i] = 0.0;
+    row[0] = tl->gs[0];
+    row[1] = tl->gs[1];
+    row[2] = tl->gs[2];
     int last = -1, first = G;
-    for (int c = lane; c < G; c += 32)
+    for (int c = 0; c < G; ++c)
       if (tl->cflag[c]) {
         last = c;
         if (first == G) first = c;
       }
+    row[3] = last >= 0 ? 1.0 : 0.0;
+    for (int c = (last < 0 ? 0 : last); c < G; ++c)
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      last = max(last, __shfl_xor_sync(0xffffffffu, last, d));
-      first = min(first, __shfl_xor_sync(0xffffffffu, first, d));
+      for (int i = 0; i < 6; ++i) row[4 + i] = __dadd_rn(row[4 + i], tl->gbuf[c][4 + i]);
+    if constexpr (FG) {
+      const int end = first == G ? G - 1 : first;
+      for (int c = 0; c <= end; ++c)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) row[10 + i] = __dadd_rn(row[10 + i], tl->gbuf[c][10 + i]);
     }
-    const int c0 = last < 0 ? 0 : last, c1 = first == G ? G - 1 : first;
-    double v[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) v[i] = 0.0;
-    for (int c = c0 + lane; c < G; c += 32)
-#pragma unroll
-      for (int i = 0; i < 6; ++i) v[i] = __dadd_rn(v[i], tl->gbuf[c][4 + i]);
-    if constexpr (FG)
-      for (int c = lane; c <= c1; c += 32)
-#pragma unroll
-        for (int i = 0; i < 6; ++i) v[6 + i] = __dadd_rn(v[6 + i], tl->gbuf[c][10 + i]);
-#pragma unroll
-    for (int i = 0; i < 12; ++i) v[i] = warp_sum(v[i]);
-    double x = 0.0;  // lane i holds row element i
-    if (lane < 3) x = tl->gs[lane];
-    if (lane == 3) x = last >= 0 ? 1.0 : 0.0;
-#pragma unroll
-    for (int i = 0; i < 12; ++i)
-      if (lane == 4 + i) x = v[i];
-    if (lane == 16) x = aux0;
-    if (lane == 17) x = aux1;
-    if (lane < 18)
-      for (int q = 0; q < R; ++q) tl->xpay[q][(slot + me) * kXrStride + lane] = x;
-    __syncwarp();
-    // system-scope release reduction by lane 0, cumulative over the warp's
-    // row stores (ordered before it by the warp barrier)
-    if (lane == 0) {
-      if (P.xr_sys)  // peers on other GPUs (NVLink): system scope
-        for (int q = 0; q < R; ++q)
-          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(tl->xbar[q]) : "memory");
-      else  // every shard on this device: gpu scope suffices
-        for (int q = 0; q < R; ++q)
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tl->xbar[q]) : "memory");
+    row[16] = aux0;
+    row[17] = aux1;
+    for (int q = 0; q < R; ++q) {
+      double* dst = P.xr_pay[q] + (slot + me) * kXrStride;
+      for (int i = 0; i < 18; ++i) dst[i] = row[i];
     }
+    // release-reduction at system scope: orders this thread's row stores
+    // before the arrival (no separate fence round trip)
+    if (P.xr_sys)  // peers on other GPUs (NVLink): system scope
+      for (int q = 0; q < R; ++q)
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(P.xr_bar[q]) : "memory");
+    else  // every shard on this device: gpu scope suffices
+      for (int q = 0; q < R; ++q)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.xr_bar[q]) : "memory");
   }
   const unsigned target = static_cast<unsigned>(cs.xr_base + (xc + 1) * static_cast<unsigned long long>(R));
-  if (lane == 0) {
-    const unsigned* mybar = tl->xbar[me];
-    const unsigned long long t0 = gtimer();
-    unsigned it = 0;
-    auto arrived = [&]() { return P.xr_sys ? ld_acquire_sys_u32(mybar) : ld_acquire_u32(mybar); };
-    while (static_cast<int>(arrived() - target) < 0) {
-      if ((++it & 1023u) == 0 && gtimer() - t0 > 2 * kWatchdogNs)
-        watchdog_trap("cross-shard exchange", ld_acquire_sys_u32(mybar), target);
-    }
+  const unsigned* mybar = P.xr_bar[me];
+  const unsigned long long t0 = gtimer();
+  unsigned it = 0;
+  auto arrived = [&]() { return P.xr_sys ? ld_acquire_sys_u32(mybar) : ld_acquire_u32(mybar); };
+  while (static_cast<int>(arrived() - target) < 0) {
+    if ((++it & 1023u) == 0 && gtimer() - t0 > 2 * kWatchdogNs)
+      watchdog_trap("cross-shard exchange", arrived(), target);
   }
-  __syncwarp();
-  // all R rows with ONE bulk copy into shared memory (the rows were written
-  // by other SMs / GPUs; the acquire above made them visible to this thread,
-  // the proxy fence orders the async-proxy read after it)
-  if (lane == 0) {
-    const uint32_t bytes = static_cast<uint32_t>(R) * kXrStride * 8u;
-    fence_proxy_async_global();
-    mbar_arrive_expect_tx(&tl->xmbar, bytes);
-    bulk_load_1d(&tl->xrows[0][0], tl->xpay[me] + slot * kXrStride, bytes, &tl->xmbar);
-  }
-  mbar_wait(&tl->xmbar, tl->xphase);
-  __syncwarp();
-  if (lane == 0) tl->xphase ^= 1u;
-  double r[18];
-#pragma unroll
-  for (int i = 0; i < 18; ++i) r[i] = lane < R ? tl->xrows[lane][i] : 0.0;
-  // fixed-order folds over shards (lane order = rank order)
+  const double* rows = P.xr_pay[me] + slot * kXrStride;
   double g0 = 0.0, g1 = 0.0, g2 = 0.0, a0 = 0.0, a1 = 0.0;
   for (int q = 0; q < R; ++q) {
-    g0 = __dadd_rn(g0, __shfl_sync(0xffffffffu, r[0], q));
-    g1 = __dadd_rn(g1, __shfl_sync(0xffffffffu, r[1], q));
-    g2 = __dadd_rn(g2, __shfl_sync(0xffffffffu, r[2], q));
-    a0 = fmax(a0, __shfl_sync(0xffffffffu, r[16], q));
-    a1 = fmax(a1, __shfl_sync(0xffffffffu, r[17], q));
+    const double* r = rows + size_t(q) * kXrStride;
+    g0 = __dadd_rn(g0, __ldcv(r + 0));
+    g1 = __dadd_rn(g1, __ldcv(r + 1));
+    g2 = __dadd_rn(g2, __ldcv(r + 2));
+    a0 = fmax(a0, __ldcv(r + 16));
+    a1 = fmax(a1, __ldcv(r + 17));
   }
+  tl->gs[0] = g0;
+  tl->gs[1] = g1;
+  tl->gs[2] = g2;
+  tl->xaux[0] = a0;
+  tl->xaux[1] = a1;
   // fwd: tails of shards start .. me-1 (start = the last earlier shard with a
   // stratum start); rev: heads of shards me+1 .. end (end = the first later
   // shard with a stratum start)
-  const unsigned flags = __ballot_sync(0xffffffffu, lane < R && r[3] != 0.0);
-  const unsigned below = flags & ((1u << me) - 1u);
-  const int start = below ? 31 - __clz(below) : 0;
-  const unsigned above = me + 1 < 32 ? (flags & ~((2u << me) - 1u)) : 0u;
-  const int end = above ? __ffs(above) - 1 : R - 1;
-  double f[12];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) f[i] = 0.0;
+  int start = 0;
+  for (int q = me - 1; q >= 0; --q)
+    if (__ldcv(rows + size_t(q) * kXrStride + 3) != 0.0) {
+      start = q;
+      break;
+    }
+  double f[6] = {0, 0, 0, 0, 0, 0};
   for (int q = start; q < me; ++q)
 #pragma unroll
-    for (int i = 0; i < 6; ++i) f[i] = __dadd_rn(f[i], __shfl_sync(0xffffffffu, r[4 + i], q));
-  if constexpr (FG)
+    for (int i = 0; i < 6; ++i) f[i] = __dadd_rn(f[i], __ldcv(rows + size_t(q) * kXrStride + 4 + i));
+#pragma unroll
+  for (int i = 0; i < 6; ++i) tl->xext[i] = f[i];
+  if constexpr (FG) {
+    int end = R - 1;
+    for (int q = me + 1; q < R; ++q)
+      if (__ldcv(rows + size_t(q) * kXrStride + 3) != 0.0) {
+        end = q;
+        break;
+      }
+    double r6[6] = {0, 0, 0, 0, 0, 0};
     for (int q = me + 1; q <= end; ++q)
 #pragma unroll
-      for (int i = 0; i < 6; ++i) f[6 + i] = __dadd_rn(f[6 + i], __shfl_sync(0xffffffffu, r[10 + i], q));
-  if (lane == 0) {
-    tl->gs[0] = g0;
-    tl->gs[1] = g1;
-    tl->gs[2] = g2;
-    tl->xaux[0] = a0;
-    tl->xaux[1] = a1;
+      for (int i = 0; i < 6; ++i)
+        r6[i] = __dadd_rn(r6[i], __ldcv(rows + size_t(q) * kXrStride + 10 + i));
 #pragma unroll
-    for (int i = 0; i < 12; ++i) tl->xext[i] = f[i];
-    cs.xr_count = xc + 1;
+    for (int i = 0; i < 6; ++i) tl->xext[6 + i] = r6[i];
   }
-  __syncwarp();
+  cs.xr_count = xc + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1908,8 +1879,8 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   auto xshard = [&](double aux0, double aux1) {
     if (P.nranks <= 1) return;
     __syncwarp();
-    cross_shard<FG>(P, tl, cta, lane, __shfl_sync(0xffffffffu, aux0, 0),
-                    __shfl_sync(0xffffffffu, aux1, 0));
+    if (lane == 0) cross_shard<FG>(P, tl, cta, aux0, aux1);
+    __syncwarp();
   };
   auto publish_full = [&](double p0, double p1, double pb, int auxmode = 0) {
     double* pm = wbuf();
@@ -2178,10 +2149,12 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       }
       if (P.nranks > 1) {  // OR over shards (validate-before-mutate on every shard)
         __syncwarp();
-        if (lane == 0) tl->gs[0] = tl->gs[1] = tl->gs[2] = 0.0;
+        if (lane == 0) {
+          tl->gs[0] = tl->gs[1] = tl->gs[2] = 0.0;
+          cross_shard<FG>(P, tl, cta, 0.0, anyd);
+          anyd = tl->xaux[1];
+        }
         __syncwarp();
-        cross_shard<FG>(P, tl, cta, lane, 0.0, __shfl_sync(0xffffffffu, anyd, 0));
-        if (lane == 0) anyd = tl->xaux[1];
       }
       if (lane == 0) {
         const bool any = anyd != 0.0;
@@ -2333,12 +2306,6 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       mbar_init(&tl->empty[s], 1);
     }
     mbar_init(&tl->gbar, 1);
-    mbar_init(&tl->xmbar, 1);
-    tl->xphase = 0u;
-    for (int q = 0; q < P.nranks && q < 16; ++q) {  // pointer tables: no dependent loads later
-      tl->xpay[q] = P.xr_pay[q];
-      tl->xbar[q] = P.xr_bar[q];
-    }
     tl->gphase = 0u;
     tl->issued = 0u;
     fence_mbar_init();
