@@ -627,12 +627,16 @@ def run_c5(args, dist):
     t = np.asarray(sim.times) + float(world - 1 - rank) * 1.0e6
     ds = capi.Dataset(t, sim.status, sim.col_ptr, sim.row_idx, device=dev)
     eng = capi.Engine(ds, "cox")
-    if world > 1:
+    if world > 1:  # CUDA-IPC exchange buffers connected through torch.distributed
         import torch.distributed as tdist
-        box = [capi.comm_unique_id() if rank == 0 else None]
-        tdist.broadcast_object_list(box, src=0)
-        comm = capi.comm_init(world, rank, box[0], dev)
+        comm = capi.comm_create(world, rank, dev)
+        handles = [None] * world
+        tdist.all_gather_object(handles, capi.comm_ipc_handle(comm))
+        capi.comm_connect(comm, handles)
         eng.attach_comm(comm)
+        fixed = [None] * world
+        tdist.all_gather_object(fixed, eng.fixed_terms())
+        eng.set_fixed_terms(np.sum(np.stack(fixed), axis=0))
     W, K = 1, 2
     dist.barrier()
     r = eng.fit(penalty="l1", strength=args.strength, tol=1e-300, max_cycles=W + K)

@@ -264,6 +264,14 @@ int gss_engine_update_validate(gss_engine* e, int64_t column, double delta, int3
  *                       the rank-ordered sums over shards (NCCL all-gather)
  */
 typedef struct gss_comm gss_comm;
+/* NCCL-free bootstrap (any out-of-band all-gather, e.g. torch.distributed /
+ * MPI): create -> export this rank's 128-byte CUDA-IPC handle -> all-gather
+ * (rank order) -> connect.  Fixed terms: all-gather gss_engine_get_fixed_terms,
+ * sum in rank order, gss_engine_set_fixed_terms on every rank. */
+int gss_comm_create(int nranks, int rank, int device, gss_comm** out);
+int gss_comm_ipc_handle(gss_comm* c, unsigned char* out128);
+int gss_comm_connect(gss_comm* c, const unsigned char* all_handles);
+int gss_engine_set_fixed_terms(gss_engine* e, const double* in, int64_t p);
 int gss_comm_unique_id(unsigned char* out128);
 int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device, gss_comm** out);
 int gss_comm_local(gss_engine* const* shards, int count, gss_comm** comms_out);

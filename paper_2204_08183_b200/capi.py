@@ -203,6 +203,10 @@ class Engine:
         self._comm = comm
         return self
 
+    def set_fixed_terms(self, fixed):
+        f = np.ascontiguousarray(fixed, np.float64)
+        check(lib().gss_engine_set_fixed_terms(self.h, _p(f), ctypes.c_int64(len(f))))
+
     def set_grid(self, grid):
         """CTAs per launch (0 = one per SM); re-partitions the tile ranges."""
         check(lib().gss_engine_set_grid(self.h, int(grid)))
@@ -363,6 +367,27 @@ def comm_init(nranks: int, rank: int, uid: bytes, device: int = 0) -> Comm:
     h = ctypes.c_void_p()
     check(lib().gss_comm_init(int(nranks), int(rank), buf, int(device), ctypes.byref(h)))
     return Comm(h)
+
+
+def comm_create(nranks: int, rank: int, device: int = 0) -> Comm:
+    """gss_comm_create: this rank's exchange buffers (NCCL-free bootstrap)."""
+    h = ctypes.c_void_p()
+    check(lib().gss_comm_create(int(nranks), int(rank), int(device), ctypes.byref(h)))
+    return Comm(h)
+
+
+def comm_ipc_handle(comm: Comm) -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    check(lib().gss_comm_ipc_handle(comm.h, buf))
+    return bytes(buf)
+
+
+def comm_connect(comm: Comm, handles) -> Comm:
+    """gss_comm_connect: `handles` = every rank's 128-byte handle, rank order."""
+    allb = b"".join(handles)
+    buf = (ctypes.c_ubyte * len(allb)).from_buffer_copy(allb)
+    check(lib().gss_comm_connect(comm.h, buf))
+    return comm
 
 
 def comm_local(engines):

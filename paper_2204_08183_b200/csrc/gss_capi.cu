@@ -1047,6 +1047,16 @@ int gss_engine_get_fixed_terms(gss_engine* E, double* out, int64_t p) {
   return GSS_OK;
 }
 
+int gss_engine_set_fixed_terms(gss_engine* E, const double* in, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (!in && p) return fail(GSS_ERR_DOMAIN, "null argument");
+  if (p != E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "fixed terms: size mismatch");
+  if (p) GSS_CUDA(cudaMemcpyAsync(E->fixed, in, p * sizeof(double), cudaMemcpyHostToDevice, E->stream));
+  GSS_CUDA(cudaStreamSynchronize(E->stream));
+  return GSS_OK;
+}
+
 int gss_engine_get_ipcw(gss_engine* E, double* u, double* g, int64_t n) {
   int rc = check_engine(E);
   if (rc) return rc;

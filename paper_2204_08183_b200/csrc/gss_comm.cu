@@ -114,6 +114,7 @@ int upload_ptrs(gss_comm* c, const std::vector<double*>& pay, const std::vector<
 extern "C" {
 
 int gss_comm_local_finalize(gss_engine* const* shards, int count);
+void gss_comm_destroy(gss_comm* c);
 
 int gss_comm_unique_id(unsigned char* out128) {
   if (!out128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
@@ -123,20 +124,76 @@ int gss_comm_unique_id(unsigned char* out128) {
   return r == 0 ? GSS_OK : set_last_error(GSS_ERR_CUDA, "ncclGetUniqueId failed");
 }
 
-int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device, gss_comm** out) {
-  if (!out || !uid128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
+// ---- NCCL-free bootstrap: the caller all-gathers the 128-byte handles ------
+struct Handles {
+  cudaIpcMemHandle_t pay, bar;
+};
+static_assert(sizeof(Handles) == 128, "two CUDA IPC handles");
+
+int gss_comm_create(int nranks, int rank, int device, gss_comm** out) {
+  if (!out) return set_last_error(GSS_ERR_DOMAIN, "null argument");
   *out = nullptr;
   if (nranks < 1 || rank < 0 || rank >= nranks)
-    return set_last_error(GSS_ERR_DOMAIN, "gss_comm_init: rank outside [0, nranks)");
-  NcclApi& a = nccl();
-  InitFn init = nccl_init_fn();
-  if (!init || !a.allgather) return set_last_error(GSS_ERR_CUDA, "gss_comm_init: libnccl not found");
+    return set_last_error(GSS_ERR_DOMAIN, "gss_comm_create: rank outside [0, nranks)");
   if (cudaSetDevice(device) != cudaSuccess)
-    return set_last_error(GSS_ERR_NO_DEVICE, "gss_comm_init: no such CUDA device");
+    return set_last_error(GSS_ERR_NO_DEVICE, "gss_comm_create: no such CUDA device");
   auto* c = new gss_comm;
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
+  if (int rc = alloc_rank_buffers(c)) {
+    gss_comm_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return GSS_OK;
+}
+
+int gss_comm_ipc_handle(gss_comm* c, unsigned char* out128) {
+  if (!c || !out128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
+  cudaSetDevice(c->device);
+  Handles h{};
+  if (cudaIpcGetMemHandle(&h.pay, c->pay) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h.bar, c->bar) != cudaSuccess)
+    return set_last_error(GSS_ERR_CUDA, "cudaIpcGetMemHandle failed");
+  std::memcpy(out128, &h, sizeof(h));
+  return GSS_OK;
+}
+
+int gss_comm_connect(gss_comm* c, const unsigned char* all128) {
+  if (!c || !all128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
+  cudaSetDevice(c->device);
+  const int R = c->nranks;
+  std::vector<double*> pay(static_cast<size_t>(R));
+  std::vector<unsigned int*> bar(static_cast<size_t>(R));
+  for (int q = 0; q < R; ++q) {
+    if (q == c->rank) {
+      pay[q] = c->pay;
+      bar[q] = c->bar;
+      continue;
+    }
+    Handles h;
+    std::memcpy(&h, all128 + size_t(q) * sizeof(Handles), sizeof(Handles));
+    void *pp = nullptr, *pb = nullptr;
+    if (cudaIpcOpenMemHandle(&pp, h.pay, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&pb, h.bar, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return set_last_error(GSS_ERR_CUDA, "cudaIpcOpenMemHandle failed (no peer access?)");
+    c->opened.push_back(pp);
+    c->opened.push_back(pb);
+    pay[q] = static_cast<double*>(pp);
+    bar[q] = static_cast<unsigned int*>(pb);
+  }
+  return upload_ptrs(c, pay, bar);
+}
+
+int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device, gss_comm** out) {
+  if (!out || !uid128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
+  *out = nullptr;
+  NcclApi& a = nccl();
+  InitFn init = nccl_init_fn();
+  if (!init || !a.allgather) return set_last_error(GSS_ERR_CUDA, "gss_comm_init: libnccl not found");
+  gss_comm* c = nullptr;
+  if (int rc = gss_comm_create(nranks, rank, device, &c)) return rc;
   auto bail = [&](int rc) {
     gss_comm_destroy(c);
     return rc;
@@ -145,43 +202,19 @@ int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device,
   std::memcpy(uid.internal, uid128, sizeof(uid.internal));
   if (init(&c->nccl, nranks, uid, rank) != 0)
     return bail(set_last_error(GSS_ERR_CUDA, "ncclCommInitRank failed"));
-  if (int rc = alloc_rank_buffers(c)) return bail(rc);
-  // export both allocations, all-gather the handles over NCCL
-  struct Handles {
-    cudaIpcMemHandle_t pay, bar;
-  } mine{};
-  if (cudaIpcGetMemHandle(&mine.pay, c->pay) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine.bar, c->bar) != cudaSuccess)
-    return bail(set_last_error(GSS_ERR_CUDA, "cudaIpcGetMemHandle failed"));
+  unsigned char mine[sizeof(Handles)];
+  if (int rc = gss_comm_ipc_handle(c, mine)) return bail(rc);
   void *d_mine = nullptr, *d_all = nullptr;
   cudaMalloc(&d_mine, sizeof(Handles));
   cudaMalloc(&d_all, sizeof(Handles) * nranks);
-  cudaMemcpy(d_mine, &mine, sizeof(Handles), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_mine, mine, sizeof(Handles), cudaMemcpyHostToDevice);
   const int rc = a.allgather(d_mine, d_all, sizeof(Handles), kNcclUint8, c->nccl, nullptr);
-  std::vector<Handles> h(static_cast<size_t>(nranks));
-  cudaMemcpy(h.data(), d_all, sizeof(Handles) * nranks, cudaMemcpyDeviceToHost);
+  std::vector<unsigned char> all(sizeof(Handles) * nranks);
+  cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost);
   cudaFree(d_mine);
   cudaFree(d_all);
-
   if (rc != 0) return bail(set_last_error(GSS_ERR_CUDA, "ncclAllGather (IPC handles) failed"));
-  std::vector<double*> pay(static_cast<size_t>(nranks));
-  std::vector<unsigned int*> bar(static_cast<size_t>(nranks));
-  for (int q = 0; q < nranks; ++q) {
-    if (q == rank) {
-      pay[q] = c->pay;
-      bar[q] = c->bar;
-      continue;
-    }
-    void *pp = nullptr, *pb = nullptr;
-    if (cudaIpcOpenMemHandle(&pp, h[q].pay, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&pb, h[q].bar, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
-      return bail(set_last_error(GSS_ERR_CUDA, "cudaIpcOpenMemHandle failed (no peer access?)"));
-    c->opened.push_back(pp);
-    c->opened.push_back(pb);
-    pay[q] = static_cast<double*>(pp);
-    bar[q] = static_cast<unsigned int*>(pb);
-  }
-  if (int rc2 = upload_ptrs(c, pay, bar)) return bail(rc2);
+  if (int rc2 = gss_comm_connect(c, all.data())) return bail(rc2);
   *out = c;
   return GSS_OK;
 }

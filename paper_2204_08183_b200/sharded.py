@@ -259,19 +259,27 @@ def fit_in_kernel_local(ds, world: int, device: int = 0, penalty="l1", strength=
 
 
 def fit_in_kernel_distributed(ds, penalty="l1", strength=0.0, tol=1e-6, max_cycles=1000,
-                              device=None, recompute_interval: int = 100):
-    """Config C5, one process per GPU (torchrun): rank r fits shard r; the NCCL
-    bootstrap id is broadcast with torch.distributed, then the exchange runs
-    over CUDA-IPC peer memory inside the kernels."""
+                              device=None, recompute_interval: int = 100, grid: int = 0):
+    """Config C5, one process per GPU (torchrun; any torch.distributed
+    backend): rank r fits shard r.  The ranks all-gather their CUDA-IPC
+    exchange-buffer handles and fixed terms with torch.distributed (no NCCL
+    needed), then the exchange runs over peer memory inside the kernels."""
     import torch.distributed as dist
     world, rank = dist.get_world_size(), dist.get_rank()
     dev = device if device is not None else __import__("torch").cuda.current_device()
-    box = [capi.comm_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0)
-    comm = capi.comm_init(world, rank, box[0], dev)
+    comm = capi.comm_create(world, rank, dev)
+    handles = [None] * world
+    dist.all_gather_object(handles, capi.comm_ipc_handle(comm))
+    capi.comm_connect(comm, handles)
     (eng,), bounds = shard_engines(ds, world, dev, ranks=[rank],
                                    recompute_interval=recompute_interval)
+    if grid:
+        eng.set_grid(grid)
     eng.attach_comm(comm)
+    fixed = [None] * world
+    dist.all_gather_object(fixed, eng.fixed_terms())
+    eng.set_fixed_terms(np.sum(np.stack(fixed), axis=0))  # rank-order sum (numpy: sequential)
+    dist.barrier()
     r = eng.fit(penalty=penalty, strength=strength, tol=tol, max_cycles=max_cycles)
     r["shards"] = bounds
     return r

@@ -2,6 +2,8 @@
 sharded.py) with every shard emulated in one process (LocalExchange) must
 reproduce the unsharded computation — derivatives and log-likelihood to the
 north-star tolerance, and fits with the same cycle counts and coefficients."""
+import os
+
 import numpy as np
 import pytest
 
@@ -110,3 +112,39 @@ def test_comm_init_single_rank_bootstrap(mods):
     b = capi.Engine(d, "cox").fit(penalty="l1", strength=1.0, max_cycles=5)
     assert a["cycles"] == b["cycles"]
     np.testing.assert_array_equal(a["beta"], b["beta"])
+
+
+@pytest.mark.parametrize("world,grid", [(2, 74), (3, 49)])
+def test_multiprocess_shards_under_mps(world, grid, tmp_path):
+    """The one-process-per-shard path (CUDA-IPC exchange buffers connected
+    through torch.distributed, system-scope flags, the exchange inside every
+    rank's kernel) with all ranks on one GPU: a private MPS daemon lets the
+    ranks' kernels co-reside (grids capped).  Every rank ends with the same
+    objective; rank 0's coefficients match the unsharded fit."""
+    import json
+    import shutil
+    import subprocess
+    import sys
+    ctl = shutil.which("nvidia-cuda-mps-control")
+    if ctl is None:
+        pytest.skip("no MPS control daemon on this box")
+    env = dict(os.environ, CUDA_MPS_PIPE_DIRECTORY=str(tmp_path / "pipe"),
+               CUDA_MPS_LOG_DIRECTORY=str(tmp_path / "log"))
+    os.makedirs(env["CUDA_MPS_PIPE_DIRECTORY"])
+    os.makedirs(env["CUDA_MPS_LOG_DIRECTORY"])
+    subprocess.run([ctl, "-d"], env=env, check=True)
+    try:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        port = 29600 + world
+        out = subprocess.run(
+            [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+             f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+             os.path.join(root, "tools", "c5_multiproc.py"), "--same-gpu", "--grid", str(grid)],
+            env=env, capture_output=True, text=True, timeout=240, cwd=root)
+    finally:
+        subprocess.run([ctl], input="quit\n", env=env, text=True)
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert out.returncode == 0 and len(lines) == world, out.stderr[-2000:]
+    assert len({ln["objective"] for ln in lines}) == 1
+    r0 = [ln for ln in lines if ln["rank"] == 0][0]
+    assert r0["pass"], r0

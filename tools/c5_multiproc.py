@@ -1,0 +1,46 @@
+"""Config C5 multi-process path (one process per shard, CUDA-IPC peer buffers,
+the exchange inside the kernels) checked against the unsharded fit.  Runs
+under torchrun with any backend; several ranks may share one GPU when an MPS
+daemon runs (each rank's grid is capped so the shards' kernels co-reside):
+
+    torchrun --nproc-per-node 2 tools/c5_multiproc.py --same-gpu --grid 74
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--same-gpu", action="store_true")
+ap.add_argument("--grid", type=int, default=0)
+ap.add_argument("--n", type=int, default=60_000)
+ap.add_argument("--p", type=int, default=8)
+ap.add_argument("--tol", type=float, default=1e-12)
+a = ap.parse_args()
+
+import torch.distributed as dist  # noqa: E402
+
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+dev = 0 if a.same_gpu else int(os.environ.get("LOCAL_RANK", "0"))
+from paper_2204_08183_b200 import capi, sharded  # noqa: E402
+from tests.test_gpu_parity import _random_sorted  # noqa: E402
+
+ds = _random_sorted(a.n, a.p, 0.05, seed=123, quant=40.0, strata=3)
+r = sharded.fit_in_kernel_distributed(ds, penalty="l1", strength=1.5, tol=a.tol, max_cycles=8,
+                                      device=dev, recompute_interval=7, grid=a.grid)
+out = {"rank": rank, "world": world, "cycles": r["cycles"], "objective": r["objective"]}
+if rank == 0:
+    one = capi.Engine(capi.Dataset.from_sorted(ds, device=dev), "cox", 7).fit(
+        penalty="l1", strength=1.5, tol=a.tol, max_cycles=8)
+    err = float(np.max(np.abs(r["beta"] - one["beta"]) / np.maximum(1.0, np.abs(one["beta"]))))
+    out.update({"unsharded_cycles": one["cycles"], "max_rel_err_beta": err,
+                "pass": bool(err < 1e-8 and one["cycles"] == r["cycles"])})
+print(json.dumps(out), flush=True)
+dist.barrier()
+dist.destroy_process_group()
