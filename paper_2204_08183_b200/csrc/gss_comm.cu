@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -311,7 +312,11 @@ int gss_engine_attach_comm(gss_engine* e, gss_comm* c) {
       for (int64_t j = 0; j < p; ++j) sum[j] += h[size_t(q) * p + j];
     cudaMemcpy(fx, sum.data(), sum.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
-  return gss::engine_attach_comm(e, c->nranks, c->rank, c->d_pay, c->d_bar, c->sys_scope ? 1 : 0);
+  // GSS_XR_SCOPE=gpu: every rank is known to share one device (e.g. several
+  // shard processes on one GPU under MPS): gpu-scope flags are sufficient
+  const char* sc = std::getenv("GSS_XR_SCOPE");
+  const bool sys = c->sys_scope && !(sc && std::strcmp(sc, "gpu") == 0);
+  return gss::engine_attach_comm(e, c->nranks, c->rank, c->d_pay, c->d_bar, sys ? 1 : 0);
 }
 
 int gss_comm_local_finalize(gss_engine* const* shards, int count) {
