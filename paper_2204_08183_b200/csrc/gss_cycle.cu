@@ -174,10 +174,7 @@ struct Tail {
   double gc[NG][16];     // the tile's carries (group exchange)
   double wpart[W][4];
   unsigned int progress[NG];
-  SlotState ssb[2];        // slot state, double-buffered by slot parity: the control warp
-                           // prepares slot k+1 while the consumers may still read slot k
-  unsigned fields_seq;     // k+1: slot k's static fields (and run-ahead flag) are published
-  unsigned resolved_seq;   // k+1: slot k's step-dependent state (pending update, carries)
+  SlotState ss;
   double bcast[8];
   double gs[16];
   uint8_t cflag[256];   // CTA range holds a stratum-first tile (grid <= 256)
@@ -1580,8 +1577,7 @@ __device__ __forceinline__ void gather_warp(const CycleParams& P, const double* 
 
 // corrected CTA carries from the gathered sums (thread 0)
 template <bool FG>
-__device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl, SlotState& dst,
-                                             double k1) {
+__device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl, double k1) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     double v = __dadd_rn(tl->gs[3 + i], __dmul_rn(k1, tl->gs[6 + i]));
@@ -1590,7 +1586,7 @@ __device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl,
                                     : __ldcg(P.ext + i);
       v = __dadd_rn(x, v);
     }
-    dst.cin_f[i] = v;
+    tl->ss.cin_f[i] = v;
   }
   if constexpr (FG) {
 #pragma unroll
@@ -1601,7 +1597,7 @@ __device__ __forceinline__ void set_carry_in(const CycleParams& P, Tail<FG>* tl,
                                       : __ldcg(P.ext + 4 + i);
         v = __dadd_rn(v, x);
       }
-      dst.cin_r[i] = v;
+      tl->ss.cin_r[i] = v;
     }
   }
 }
@@ -1813,6 +1809,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
   constexpr int W = Gm::kW, NB = 32 * W + 32;
   const int G = P.grid;
   Ctl* ctl = P.ctl;
+  SlotState& ss = tl->ss;
   const bool prof = (P.dbg & 256) && cta == kProfCta && lane == 0;
   // phase profile in shared memory (no local-memory array)
   long long* ph = tl->cs.ph;
@@ -1918,7 +1915,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
                !(P.dbg & 8)) ? 1 : 0;
     return f;
   };
-  auto set_slot_fields = [&](SlotState& ss, const SlotFields& f) {
+  auto set_slot_fields = [&](const SlotFields& f) {
     if (!f.valid) return;
     ss.col = f.col;
     ss.ncol = f.ncol;
@@ -1954,25 +1951,20 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
     return;
   }
   if (lane == 0) {
-    SlotState& s0 = tl->ssb[0];
-    set_carry_in<FG>(P, tl, s0, 0.0);
-    s0.pcol = -1;
-    s0.delta = 0.0;
-    s0.phi = 1.0;
-    s0.pind = 1;
-    s0.refresh = 0;
-    s0.dry = err ? 1 : 0;
-    set_slot_fields(s0, slot_fields(0));
-    flag_release(&tl->fields_seq, 1u);
-    flag_release(&tl->resolved_seq, 1u);
+    set_carry_in<FG>(P, tl, 0.0);
+    ss.pcol = -1;
+    ss.delta = 0.0;
+    ss.phi = 1.0;
+    ss.pind = 1;
+    ss.refresh = 0;
+    ss.dry = err ? 1 : 0;
+    set_slot_fields(slot_fields(0));
   }
   go(kTaskNext);
   pmark(5);
 
   unsigned& qbase = cs.qbase;
   for (int k = 0; k < P.nslots; ++k) {
-    SlotState& ss = tl->ssb[k & 1];         // the slot being consumed
-    SlotState& nxs = tl->ssb[(k + 1) & 1];  // the slot prepared for the consumers next
     // step inputs and the next slot's fields: loaded while the slot streams
     long long& col = cs.col;
     long long& ncol = cs.ncol;
@@ -2134,7 +2126,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       phi = (delta != 0.0) ? exp(delta) : 1.0;
       // carries for slot k+1 (linear path; refresh / valued paths redo them)
       pmark(9);
-      set_carry_in<FG>(P, tl, nxs, __dsub_rn(phi, 1.0));
+      set_carry_in<FG>(P, tl, __dsub_rn(phi, 1.0));
       pmark(10);
     }
     need_exact = __shfl_sync(0xffffffffu, need_exact, 0);
@@ -2174,7 +2166,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
           if (cta == 0) P.halfwidth[col] = in_hw;  // unchanged on the exception path
           delta = 0.0;
           phi = 1.0;
-          set_carry_in<FG>(P, tl, nxs, 0.0);
+          set_carry_in<FG>(P, tl, 0.0);
         }
       }
     }
@@ -2214,7 +2206,7 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       }
       publish_full(0.0, 0.0, 0.0, 1);
       if (lane == 0) {
-        set_carry_in<FG>(P, tl, nxs, 0.0);
+        set_carry_in<FG>(P, tl, 0.0);
         const double* pa = raux(xi - 1);
         double mm = 0.0;
         for (int c = 0; c < G; ++c) mm = fmax(mm, __ldcg(pa + size_t(c) * kPayAux + 0));
@@ -2231,19 +2223,17 @@ __device__ __forceinline__ void control_warp(const CycleParams& P, Tail<FG>* tl,
       go(kTaskValued);
       wait_done();
       publish_full(0.0, 0.0, 0.0);
-      if (lane == 0) set_carry_in<FG>(P, tl, nxs, 0.0);
+      if (lane == 0) set_carry_in<FG>(P, tl, 0.0);
     }
     // ---- the next slot's pending update and fields ----
     if (lane == 0) {
-      nxs.pcol = (delta != 0.0 && !do_refresh) ? col : -1;
-      nxs.delta = delta;
-      nxs.phi = phi;
-      nxs.pind = in_ind;
-      nxs.refresh = do_refresh;
-      nxs.dry = err ? 1 : 0;
-      set_slot_fields(nxs, nf);
-      flag_release(&tl->fields_seq, static_cast<unsigned>(k + 2));
-      flag_release(&tl->resolved_seq, static_cast<unsigned>(k + 2));
+      ss.pcol = (delta != 0.0 && !do_refresh) ? col : -1;
+      ss.delta = delta;
+      ss.phi = phi;
+      ss.pind = in_ind;
+      ss.refresh = do_refresh;
+      ss.dry = err ? 1 : 0;
+      set_slot_fields(nf);
     }
     pmark(3);
     if ((P.dbg & 65536) && lane == 0) cs.tgo = gtimer();
@@ -2316,8 +2306,6 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
       mbar_init(&tl->empty[s], 1);
     }
     mbar_init(&tl->gbar, 1);
-    tl->fields_seq = 0u;
-    tl->resolved_seq = 0u;
     tl->gphase = 0u;
     tl->issued = 0u;
     fence_mbar_init();
@@ -2366,6 +2354,7 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   }
   const bool rec_ok = (P.mode == kModeCcd || P.reuse_records) && ctl->rec_valid &&
                       ctl->rec_col == P.slot_col[0];
+  SlotState& ss = tl->ss;
   if (warp == W) {
     control_warp<FG>(P, tl, cta, t0, tc, lane);
     return;
@@ -2390,7 +2379,6 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
   int gpar = 0;        // this warp's group: mask buffer of its next tile
   const int nsl = (tl->task == kTaskExit) ? 0 : P.nslots;
   for (int k = 0; k < nsl; ++k) {
-    const SlotState& ss = tl->ssb[k & 1];
     double acc0 = 0.0, acc1 = 0.0;
     int bad = 0;
     const bool dry = ss.dry != 0;
