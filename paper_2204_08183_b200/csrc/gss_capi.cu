@@ -1343,6 +1343,8 @@ int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_s
     if (queue.empty()) continue;
     const int maxg = engines[queue[0]]->max_grid;
     int slots = max_active > 0 ? max_active : kMaxBatch;
+    if (max_active <= 0)
+      if (const char* a = std::getenv("GSS_BATCH_ACTIVE")) slots = std::max(1, std::atoi(a));
     slots = std::max(1, std::min({slots, kMaxBatch, maxg, static_cast<int>(queue.size())}));
     const int share = std::max(1, maxg / slots);
     size_t next = 0;
