@@ -1346,7 +1346,12 @@ int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_s
     if (max_active <= 0)
       if (const char* a = std::getenv("GSS_BATCH_ACTIVE")) slots = std::max(1, std::atoi(a));
     slots = std::max(1, std::min({slots, kMaxBatch, maxg, static_cast<int>(queue.size())}));
-    const int share = std::max(1, maxg / slots);
+    // CTAs per fit: with the default concurrency every fit gets maxg / kMaxBatch
+    // CTAs whatever the batch holds, so a fit's CTA partition (hence its
+    // summation order) never depends on how many fits share its launch: CV and
+    // bootstrap results are bit-identical across worker and device counts (the
+    // reference's guarantee, tests/acceptance.cpp:346-383)
+    const int share = std::max(1, maxg / (max_active > 0 ? slots : kMaxBatch));
     size_t next = 0;
     std::vector<int64_t> active;
     auto finish = [&](int64_t i, int rc) {

@@ -215,3 +215,28 @@ def test_bootstrap_parity_with_reference_module(ss, ref, name, model, lam, coef)
     # the per-resample draws, too (resample-ordered pieces of the rank driver)
     draws = ss.bootstrap_run(a, model, "l1", lam, [], coef, list(range(120)), 23, 1e-10, 500)
     assert tuple(ss.bootstrap_merge(draws, 120)) == (la, ha, fa)
+
+
+def test_cross_validate_bit_identical_across_device_lists():
+    """Acceptance #10 of the reference (tests/acceptance.cpp:346-383: results
+    bit-identical across worker counts), on the device: the same CV run with
+    its tasks dealt over 1, 2 or 3 device lanes (worker threads on GPU 0)
+    gives identical curves, selection and final coefficients."""
+    import survscan
+    rng = np.random.default_rng(11)
+    n, p = 6000, 10
+    k = int(n * p * 0.05)
+    rows, cols = rng.integers(0, n, k), rng.integers(0, p, k)
+    key = np.unique(cols * n + rows)
+    t = np.ceil(rng.exponential(size=n) * 30) / 30
+    s = (rng.random(n) < 0.7).astype(np.int64)
+    ds = survscan.dataset_from_coo(t, s, key % n, key // n, np.ones(len(key)), p,
+                                   rng.integers(0, 3, n))
+    kw = dict(model="cox", penalty="l1", grid=[0.5, 1.0, 2.0, 4.0, 8.0], folds=5, repetitions=2,
+              seed=3)
+    outs = [survscan.cross_validate(ds, devices=d, **kw) for d in ([0], [0, 0], [0, 0, 0])]
+    for o in outs[1:]:
+        assert o["selected"] == outs[0]["selected"]
+        assert [c["mean_loglik"] for c in o["curve"]] == [c["mean_loglik"] for c in outs[0]["curve"]]
+        assert np.array_equal(np.asarray(o["final_fit"]["beta"]),
+                              np.asarray(outs[0]["final_fit"]["beta"]))
