@@ -634,9 +634,11 @@ def run_c5(args, dist):
         tdist.all_gather_object(handles, capi.comm_ipc_handle(comm))
         capi.comm_connect(comm, handles)
         eng.attach_comm(comm)
-        fixed = [None] * world
+        fixed, cmax = [None] * world, [None] * world
         tdist.all_gather_object(fixed, eng.fixed_terms())
+        tdist.all_gather_object(cmax, eng.colmax())
         eng.set_fixed_terms(np.sum(np.stack(fixed), axis=0))
+        eng.set_colmax(np.max(np.stack(cmax), axis=0))
     W, K = 1, 2
     dist.barrier()
     r = eng.fit(penalty="l1", strength=args.strength, tol=1e-300, max_cycles=W + K)

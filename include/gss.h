@@ -272,6 +272,11 @@ int gss_comm_create(int nranks, int rank, int device, gss_comm** out);
 int gss_comm_ipc_handle(gss_comm* c, unsigned char* out128);
 int gss_comm_connect(gss_comm* c, const unsigned char* all_handles);
 int gss_engine_set_fixed_terms(gss_engine* e, const double* in, int64_t p);
+/* max |x| per column of the engine's dataset (the fast overflow bound); shards
+ * must share the global maximum: all-gather, max, set on every rank (the
+ * setter writes the dataset's bound, shared by its engines) */
+int gss_engine_get_colmax(gss_engine* e, double* out, int64_t p);
+int gss_engine_set_colmax(gss_engine* e, const double* in, int64_t p);
 int gss_comm_unique_id(unsigned char* out128);
 int gss_comm_init(int nranks, int rank, const unsigned char* uid128, int device, gss_comm** out);
 int gss_comm_local(gss_engine* const* shards, int count, gss_comm** comms_out);

@@ -203,6 +203,15 @@ class Engine:
         self._comm = comm
         return self
 
+    def colmax(self):
+        out = np.zeros(self.ds.p)
+        check(lib().gss_engine_get_colmax(self.h, _p(out), ctypes.c_int64(self.ds.p)))
+        return out
+
+    def set_colmax(self, cm):
+        c = np.ascontiguousarray(cm, np.float64)
+        check(lib().gss_engine_set_colmax(self.h, _p(c), ctypes.c_int64(len(c))))
+
     def set_fixed_terms(self, fixed):
         f = np.ascontiguousarray(fixed, np.float64)
         check(lib().gss_engine_set_fixed_terms(self.h, _p(f), ctypes.c_int64(len(f))))

@@ -1057,6 +1057,25 @@ int gss_engine_set_fixed_terms(gss_engine* E, const double* in, int64_t p) {
   return GSS_OK;
 }
 
+// max |x| per column (the fast overflow bound): patient shards must share
+// the global bound so every shard takes the same validate-before-mutate path
+int gss_engine_get_colmax(gss_engine* E, double* out, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (p != E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "colmax: size mismatch");
+  if (p) GSS_CUDA(cudaMemcpy(out, E->ds->colmax, p * sizeof(double), cudaMemcpyDeviceToHost));
+  return GSS_OK;
+}
+
+int gss_engine_set_colmax(gss_engine* E, const double* in, int64_t p) {
+  int rc = check_engine(E);
+  if (rc) return rc;
+  if (!in && p) return fail(GSS_ERR_DOMAIN, "null argument");
+  if (p != E->ds->p) return fail(GSS_ERR_INVALID_COLUMN, "colmax: size mismatch");
+  if (p) GSS_CUDA(cudaMemcpy(E->ds->colmax, in, p * sizeof(double), cudaMemcpyHostToDevice));
+  return GSS_OK;
+}
+
 int gss_engine_get_ipcw(gss_engine* E, double* u, double* g, int64_t n) {
   int rc = check_engine(E);
   if (rc) return rc;

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -116,6 +117,8 @@ extern "C" {
 
 int gss_comm_local_finalize(gss_engine* const* shards, int count);
 void gss_comm_destroy(gss_comm* c);
+int gss_engine_get_colmax(gss_engine* e, double* out, int64_t p);
+int gss_engine_set_colmax(gss_engine* e, const double* in, int64_t p);
 
 int gss_comm_unique_id(unsigned char* out128) {
   if (!out128) return set_last_error(GSS_ERR_DOMAIN, "null argument");
@@ -311,6 +314,20 @@ int gss_engine_attach_comm(gss_engine* e, gss_comm* c) {
     for (int q = 0; q < c->nranks; ++q)
       for (int64_t j = 0; j < p; ++j) sum[j] += h[size_t(q) * p + j];
     cudaMemcpy(fx, sum.data(), sum.size() * sizeof(double), cudaMemcpyHostToDevice);
+    // the fast overflow bound: max over ranks
+    std::vector<double> cm(static_cast<size_t>(p));
+    if (int rc2 = gss_engine_get_colmax(e, cm.data(), p)) return rc2;
+    double* dcm = nullptr;
+    cudaMalloc(reinterpret_cast<void**>(&dcm), sizeof(double) * size_t(p) * (c->nranks + 1));
+    cudaMemcpy(dcm, cm.data(), sizeof(double) * size_t(p), cudaMemcpyHostToDevice);
+    const int rc3 = nccl().allgather(dcm, dcm + p, sizeof(double) * size_t(p), kNcclUint8, c->nccl, st);
+    cudaMemcpyAsync(h.data(), dcm + p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(dcm);
+    if (rc3 != 0) return set_last_error(GSS_ERR_CUDA, "ncclAllGather (colmax) failed");
+    for (int q = 0; q < c->nranks; ++q)
+      for (int64_t j = 0; j < p; ++j) cm[j] = std::max(cm[j], h[size_t(q) * p + j]);
+    if (int rc4 = gss_engine_set_colmax(e, cm.data(), p)) return rc4;
   }
   // GSS_XR_SCOPE=gpu: every rank is known to share one device (e.g. several
   // shard processes on one GPU under MPS): gpu-scope flags are sufficient
@@ -338,6 +355,14 @@ int gss_comm_local_finalize(gss_engine* const* shards, int count) {
   std::vector<double> sum(size_t(p0), 0.0);
   for (int r = 0; r < count; ++r)
     for (int64_t j = 0; j < p0; ++j) sum[j] += fx[r][j];
+  // the fast overflow bound: the max over shards, on every shard
+  std::vector<double> cm(static_cast<size_t>(p0), 0.0), tmp(static_cast<size_t>(p0));
+  for (int r = 0; r < count; ++r) {
+    if (int rc = gss_engine_get_colmax(shards[r], tmp.data(), p0)) return rc;
+    for (int64_t j = 0; j < p0; ++j) cm[j] = std::max(cm[j], tmp[j]);
+  }
+  for (int r = 0; r < count; ++r)
+    if (int rc = gss_engine_set_colmax(shards[r], cm.data(), p0)) return rc;
   for (int r = 0; r < count; ++r) {
     double* d = nullptr;
     int64_t p = 0;

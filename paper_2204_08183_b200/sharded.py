@@ -276,9 +276,11 @@ def fit_in_kernel_distributed(ds, penalty="l1", strength=0.0, tol=1e-6, max_cycl
     if grid:
         eng.set_grid(grid)
     eng.attach_comm(comm)
-    fixed = [None] * world
+    fixed, cmax = [None] * world, [None] * world
     dist.all_gather_object(fixed, eng.fixed_terms())
+    dist.all_gather_object(cmax, eng.colmax())
     eng.set_fixed_terms(np.sum(np.stack(fixed), axis=0))  # rank-order sum (numpy: sequential)
+    eng.set_colmax(np.max(np.stack(cmax), axis=0))  # one overflow bound on every shard
     dist.barrier()
     r = eng.fit(penalty=penalty, strength=strength, tol=tol, max_cycles=max_cycles)
     r["shards"] = bounds

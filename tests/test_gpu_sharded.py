@@ -148,3 +148,71 @@ def test_multiprocess_shards_under_mps(world, grid, tmp_path):
     assert len({ln["objective"] for ln in lines}) == 1
     r0 = [ln for ln in lines if ln["rank"] == 0][0]
     assert r0["pass"], r0
+
+
+def test_in_kernel_sharded_fit_valued_dense_and_refresh(mods):
+    """Shards of a dataset with valued columns (the exp recompute and the
+    valued-record correction exchange), a dense column (density >= 25%: the
+    dense pool), strata spanning the cuts and in-kernel refreshes every 3
+    accepted updates (max |eta| combined over shards): same cycles and
+    coefficients as the oracle."""
+    capi, sharded = mods
+    rng = np.random.default_rng(21)
+    n, p = 40_000, 6
+    rows, cols, vals = [], [], []
+    for j, dens in enumerate([0.05, 0.4, 0.03, 0.08, 0.02, 0.05]):
+        r = np.sort(rng.choice(n, size=int(dens * n), replace=False))
+        v = np.ones(r.size) if j in (2, 4) else np.round(rng.normal(size=r.size), 2) + 0.01
+        rows.append(r)
+        cols.append(np.full(r.size, j))
+        vals.append(v)
+    t = np.ceil(rng.exponential(size=n) * 30) / 30
+    st = (rng.random(n) < 0.7).astype(np.int64)
+    ds = orc.assemble(t, st, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p,
+                      strata=rng.integers(0, 3, n))
+    for world in (2, 3):
+        r = sharded.fit_in_kernel_local(ds, world, penalty="l1", strength=1.0, max_cycles=6,
+                                        recompute_interval=3)
+        ref = orc.OracleEngine(ds, "cox", recompute_interval=3).fit(
+            penalty="l1", strength=1.0, max_cycles=6)
+        assert r["cycles"] == ref["cycles"]
+        assert np.max(rel(r["beta"], ref["beta"])) < TOL_BETA
+        assert rel(r["objective"], ref["objective"]) < TOL_DERIV
+
+
+def test_in_kernel_sharded_overflow_raises_on_every_shard(mods):
+    """A step that would push |x'beta| past 700 on one row of the LAST shard
+    (a censored row with the smallest time and x = 1e5, the construction of
+    test_fit_overflow_mid_cycle_raises_like_reference) must stop the fit on
+    every shard: the exact validation's overflow flag is OR-ed over shards in
+    the kernel, and the error is the reference's OverflowError."""
+    capi, sharded = mods
+    rng = np.random.default_rng(77)
+    n, p = 30_000, 6
+    t = rng.exponential(size=n)
+    status = (rng.random(n) < 0.7).astype(np.int64)
+    last = int(np.argmin(t))
+    status[last] = 0
+    bulk = np.setdiff1d(np.arange(n), [last])
+    rows, cols, vals = [], [], []
+    eta = np.zeros(n)
+    for j in range(p):
+        r = rng.choice(bulk, size=1500, replace=False)
+        v = np.round(rng.uniform(-3.0, 3.0, size=r.size), 2)
+        v[v == 0] = 1.5
+        eta[r] += 0.4 * v
+        r = np.append(r, last)
+        v = np.append(v, 1.0e5)
+        o = np.argsort(r)
+        rows.append(r[o])
+        cols.append(np.full(r.size, j))
+        vals.append(v[o])
+    t = t / np.exp(eta)
+    t[last] = t.min() / 2.0
+    ds = orc.assemble(t, status, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), p)
+    with pytest.raises(orc.OracleError) as e_ref:
+        orc.OracleEngine(ds, "cox").fit(penalty="none", max_cycles=5)
+    for world in (2, 3):
+        with pytest.raises(capi.GssError) as e_dev:
+            sharded.fit_in_kernel_local(ds, world, penalty="none", max_cycles=5)
+        assert e_dev.value.kind == e_ref.value.kind == "OverflowError"
