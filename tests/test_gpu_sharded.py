@@ -132,7 +132,8 @@ def test_multiprocess_shards_under_mps(world, grid, tmp_path):
                CUDA_MPS_LOG_DIRECTORY=str(tmp_path / "log"))
     os.makedirs(env["CUDA_MPS_PIPE_DIRECTORY"])
     os.makedirs(env["CUDA_MPS_LOG_DIRECTORY"])
-    subprocess.run([ctl, "-d"], env=env, check=True)
+    if subprocess.run([ctl, "-d"], env=env).returncode != 0:
+        pytest.skip("could not start a private MPS daemon")
     try:
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         port = 29600 + world
