@@ -85,6 +85,27 @@ cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 
+// Engine buffers come from the device's stream-ordered memory pool (release
+// threshold raised once per device): creating and destroying hundreds of
+// fold / held-out engines (C4) neither pays cudaMalloc latency nor
+// serialises on cudaFree's implicit device synchronisation.
+template <class T>
+cudaError_t ealloc(T** p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [dev]() {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  return cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -214,11 +235,14 @@ struct gss_engine {
   ~gss_engine() {
     cudaSetDevice(ds->device);
     if (stream) cudaStreamSynchronize(stream);
+    // pool allocations (ealloc): stream-ordered frees, no device-wide sync
     for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
                     (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
                     (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
-                    (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0, (void*)sep})
-      if (q) cudaFree(q);
+                    (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0})
+      if (q) cudaFreeAsync(q, stream);
+    if (stream) cudaStreamSynchronize(stream);
+    if (sep) cudaFree(sep);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -723,26 +747,26 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
   EK(cudaEventCreate(&E->ev0));
   EK(cudaEventCreate(&E->ev1));
-  EK(dalloc(&E->eta, npad));
-  EK(dalloc(&E->e, npad));
-  EK(dalloc(&E->scratch, npad));
-  EK(dalloc(&E->code, npad));
-  EK(dalloc(&E->beta, p));
-  EK(dalloc(&E->halfwidth, p));
-  EK(dalloc(&E->fixed, p));
-  EK(dalloc(&E->penalized, p));
-  EK(dalloc(&E->trec, size_t(nt) * kRecStride));
-  EK(dalloc(&E->tcar, size_t(nt) * kCarStride));
-  EK(dalloc(&E->cpay, size_t(2) * E->grid * (kPayStride + kPayAux)));
-  EK(dalloc(&E->slot_out, size_t(p + 1) * 4));
-  EK(dalloc(&E->slot_col, size_t(p + 1)));
-  EK(dalloc(&E->bar, 1));
-  EK(dalloc(&E->ctl, 1));
-  EK(dalloc(&E->dflag, 4));
-  EK(dalloc(&E->ext, 8));
-  EK(dalloc(&E->shard, 8));
+  EK(ealloc(&E->eta, npad, E->stream));
+  EK(ealloc(&E->e, npad, E->stream));
+  EK(ealloc(&E->scratch, npad, E->stream));
+  EK(ealloc(&E->code, npad, E->stream));
+  EK(ealloc(&E->beta, p, E->stream));
+  EK(ealloc(&E->halfwidth, p, E->stream));
+  EK(ealloc(&E->fixed, p, E->stream));
+  EK(ealloc(&E->penalized, p, E->stream));
+  EK(ealloc(&E->trec, size_t(nt) * kRecStride, E->stream));
+  EK(ealloc(&E->tcar, size_t(nt) * kCarStride, E->stream));
+  EK(ealloc(&E->cpay, size_t(2) * E->grid * (kPayStride + kPayAux), E->stream));
+  EK(ealloc(&E->slot_out, size_t(p + 1) * 4, E->stream));
+  EK(ealloc(&E->slot_col, size_t(p + 1), E->stream));
+  EK(ealloc(&E->bar, 1, E->stream));
+  EK(ealloc(&E->ctl, 1, E->stream));
+  EK(ealloc(&E->dflag, 4, E->stream));
+  EK(ealloc(&E->ext, 8, E->stream));
+  EK(ealloc(&E->shard, 8, E->stream));
   EK(cudaMemsetAsync(E->ext, 0, 8 * sizeof(double), E->stream));
-  if (E->weighted) EK(dalloc(&E->g, npad));
+  if (E->weighted) EK(ealloc(&E->g, npad, E->stream));
   EK(cudaMallocHost(reinterpret_cast<void**>(&E->h_ctl), sizeof(Ctl)));
   std::memset(E->h_ctl, 0, sizeof(Ctl));
   E->h_ctl->err_col = -1;
@@ -819,7 +843,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
       const int c = std::atoi(cap);
       if (c > 0) mg = std::min(mg, c);
     }
-    EK(dalloc(&E->cta_tile0, maxg + 1));
+    EK(ealloc(&E->cta_tile0, maxg + 1, E->stream));
     E->max_grid = maxg;
     int rc2 = partition_ctas(E, std::max(1, std::min(nt, mg)));
     if (rc2) return bail(rc2);
