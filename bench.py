@@ -297,7 +297,7 @@ def roofline(n, col_ptr, cycles_ms, accepted_per_cycle, p, launches_per_cycle):
             "kernel": "cycle_kernel<false> (p coordinate slots + 1 objective slot per launch)"}
 
 
-def parity_spot_check(sim, eng, cols=(0, 1777, 4999)):
+def parity_spot_check(sim, eng, cols=(0, 1777, 4999), model="cox"):
     """CHECKER (outside every timed region): the device engine's derivatives
     and log-likelihood at the fitted beta of the timed C2 cycles against the C
     oracle (oracle/oracle.c, pinned to the reference's goldens) on the same
@@ -309,7 +309,7 @@ def parity_spot_check(sim, eng, cols=(0, 1777, 4999)):
                     np.arange(n, dtype=np.int64), np.ascontiguousarray(sim.col_ptr),
                     np.ascontiguousarray(sim.row_idx), np.ones(1), np.ones(p, np.uint8))
     t0 = time.perf_counter()
-    ref = orc.OracleEngine(ds, "cox")
+    ref = orc.OracleEngine(ds, model)
     ref.load_beta(beta)
     ll_d, ll_r = eng.log_likelihood(), ref.log_likelihood()
     eg, eh = 0.0, 0.0
@@ -552,6 +552,10 @@ def run_c3(args, dist):
     eng.fit(penalty="l1", strength=args.strength, tol=1e-300, max_cycles=W + K)
     ms, acc = eng.cycle_stats()
     timed = float(ms[W:W + K].sum())
+    parity = None
+    if dist.rank == 0 and not args.no_parity:  # checker, outside the timed cycles
+        parity = parity_spot_check(sim, eng, cols=(0, args.c3_p // 2, args.c3_p - 1),
+                                   model="finegray")
     t_max = dist.max(timed)
     value = dist.sum(float(K * args.c3_p)) / (t_max * 1e-3)
     nnz = np.diff(sim.col_ptr).astype(np.float64)
@@ -563,7 +567,7 @@ def run_c3(args, dist):
                         f"ties q=1e-3, cq={args.censoring_quantile}, L1 gamma=sqrt(2)",
             "value": round(value, 2), "unit": "coord_updates/s",
             "ms_per_cycle": round(t_max / K, 3), "cycles_timed": K,
-            "competing_rows": n_comp,
+            "competing_rows": n_comp, "parity_c3": parity,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "algorithmic_bytes_per_coordinate": round(per_coord, 1)}}
