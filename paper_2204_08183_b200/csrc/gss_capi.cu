@@ -435,6 +435,10 @@ int partition_ctas(gss_engine* E, int grid) {
   const int nt = E->ds->ntiles;
   grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
   std::vector<double> w(static_cast<size_t>(nt), 1.0);
+  // Per-tile cost model: 1 + 0.05 per transform pass.  A per-event-block-end
+  // term (GSS_BE_W; tools/tile_cost_probe.py measures ~630 consumer cycles
+  // per end on a ~6250-cycle tile) made the C2 bench slower at 0.05 / 0.1
+  // (18.1k / 17.3k vs 21.4k coord/s), so it defaults to 0.
   static const double kPassW =
       std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
   static const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
@@ -447,7 +451,8 @@ int partition_ctas(gss_engine* E, int grid) {
       work += any ? 1 : 0;
       ends += any;
     }
-    w[t] = 1.0 + kPassW * work + kBeW * double(ends) / kTileRows;
+    // (distinct event times saturate at one transform per row: cap at 4)
+    w[t] = std::min(4.0, 1.0 + kPassW * work + kBeW * double(ends));
   }
   double tot = 0.0;
   for (double x : w) tot += x;

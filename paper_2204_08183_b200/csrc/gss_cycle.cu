@@ -2412,6 +2412,11 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
           }
         }
         mbar_wait_wd(&tl->full[s], ph, "consumer full-stage wait", q, lane == 0 ? tl->mark : nullptr);
+        // per-tile cost probe (GSS_DEBUG bit 524288 + GSS_TRACE=1): cycles from
+        // stage-ready to the end of the tile, for the slot in the middle
+        const bool tprobe = GSS_ENABLE_TRACE && (P.dbg & 524288) && P.trace && k == P.nslots / 2 &&
+                            gw == 0 && lane == 0;
+        const long long tp0 = tprobe ? clock64() : 0;
         unsigned char* sb = smem + size_t(s) * Gm::kStage;
         if (!dry && !(P.dbg & 1))
           consume_tile<FG>(P, tl, sb, tl->info[s], ss, g, gw, lane, gpar, acc0, acc1, bad,
@@ -2425,6 +2430,8 @@ __global__ void __launch_bounds__(Geo<FG>::kThreads, 1)
           flag_release(&tl->progress[g], q + 1);  // the tile's record before its progress
           mbar_arrive(&tl->empty[s]);
         }
+        if (tprobe && t0 + i < static_cast<int>(P.trace_cap))
+          P.trace[t0 + i] = static_cast<unsigned long long>(clock64() - tp0);
       }
     }
     qbase += static_cast<unsigned>(tc);
