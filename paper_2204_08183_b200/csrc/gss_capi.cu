@@ -822,7 +822,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   P.vals = ds->vals;
   P.col_ind = ds->col_ind;
   P.tile_ptr = ds->tile_ptr;
-  P.dense_idx = ds->dense_idx;
+  P.dense_idx = ds->ndense ? ds->dense_idx : nullptr;  // no dense column: no per-tile lookup
   P.dense_pool = ds->dense_pool;
   P.row_ptr = ds->row_ptr;
   P.csr_col = ds->csr_col;
