@@ -430,18 +430,22 @@ double penalty_value(const gss_penalty_spec* pen, const std::vector<double>& bet
 
 // Static contiguous CTA tile ranges, balanced by estimated tile cost: a tile
 // costs its streaming (1) plus its transform passes (8-row x 32-lane passes
-// holding a tied-block end).  Sets E->grid / prm.grid / prm.cta_tile0.
+// holding a tied-block end with events).  Sets E->grid / prm.grid / prm.cta_tile0.
 int partition_ctas(gss_engine* E, int grid) {
   const int nt = E->ds->ntiles;
   grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
   std::vector<double> w(static_cast<size_t>(nt), 1.0);
-  // Per-tile cost model: 1 + 0.05 per transform pass.  A per-event-block-end
-  // term (GSS_BE_W; tools/tile_cost_probe.py measures ~630 consumer cycles
-  // per end on a ~6250-cycle tile) made the C2 bench slower at 0.05 / 0.1
-  // (18.1k / 17.3k vs 21.4k coord/s), so it defaults to 0.
+  // Per-tile cost model: 1 + 0.12 if any pass holds a transform + 0.04 per
+  // such pass.  A consumer group's tile costs the longest of its warps, so the
+  // first transform pass costs most (tools/tile_cost_probe.py: ~5.8k cycles
+  // without, ~7.9k with); the p = 512 C2-design fit measured 42.3 us per
+  // coordinate with this model vs 43.4 with 1 + 0.05 per pass and 46.0
+  // unweighted (tools/gpu_partition_sweep.sh).  A per-event-block-end term
+  // (GSS_BE_W) made the C2 bench slower at 0.05 / 0.1, so it defaults to 0.
   static const double kPassW =
-      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.05;
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.04;
   static const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
+  static const double kAnyW = std::getenv("GSS_ANY_W") ? std::atof(std::getenv("GSS_ANY_W")) : 0.12;
   for (int t = 0; t < nt; ++t) {
     int work = 0, ends = 0;
     for (int pass = 0; pass < kTileRows / 256; ++pass) {
@@ -452,7 +456,7 @@ int partition_ctas(gss_engine* E, int grid) {
       ends += any;
     }
     // (distinct event times saturate at one transform per row: cap at 4)
-    w[t] = std::min(4.0, 1.0 + kPassW * work + kBeW * double(ends));
+    w[t] = std::min(4.0, 1.0 + kPassW * work + kBeW * double(ends) + (work ? kAnyW : 0.0));
   }
   double tot = 0.0;
   for (double x : w) tot += x;
