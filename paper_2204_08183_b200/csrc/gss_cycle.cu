@@ -637,8 +637,14 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   const double* dpen = (ss.pcol >= 0 && !ss.pind) ? dense_of(ss.pcol) : nullptr;
   const double* dnxt = ss.nind ? nullptr : dense_of(ss.ncol);
 
+  // The pre-barrier list work is spread over the group's warps (each loop
+  // is one dependent chain per entry): the patch on warp 0, the scan-column
+  // bitmask from warp 1, the next-column bitmask from warp 2, the carries on
+  // the last warp.
+  const int gt1 = ((gw + GW - 1) % GW) * 32 + lane;  // warp 1 first
+  const int gt2 = ((gw + GW - 2) % GW) * 32 + lane;  // warp 2 first
   // ---- tile carries -> group smem (visible after the first group barrier) ----
-  if (gw == 0 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
+  if (gw == GW - 1 && lane < (FG ? 15 : 7)) tl->gc[g][lane] = ld_rc<FG>(car_at<FG>(P, tl, t, inf.li) + lane, inf.li);
   const double* tcv = tl->gc[g];
 
   // ---- stale tile after a refresh: reload exp(eta) from global ----
@@ -686,7 +692,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
   }
   // ---- scan-column bitmask per thread-row (xm is all-zero on entry) ----
   if (has_cur && !dcur) {
-    for (int i = gt; i < Lc.cnt; i += GT) {
+    for (int i = gt1; i < Lc.cnt; i += GT) {
       const int32_t r = list_at(lcur, Lc, P.row_idx, i);
       const int lr = static_cast<int>(r - row0);
       uint32_t w = 1u << (lr & 7);
@@ -699,7 +705,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
     }
   }
   if constexpr (FUSED) {
-    for (int i = gt; i < Ln.cnt; i += GT) {
+    for (int i = gt2; i < Ln.cnt; i += GT) {
       const int lr = static_cast<int>(list_at(lnext, Ln, P.row_idx, i) - row0);
       atomicOr(&xn[lr >> 3], 1u << (lr & 7));
     }
