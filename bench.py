@@ -500,16 +500,10 @@ def run_gss(args, dist):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (device generator, simulate_cox design family; random beta)",
-        "config": {
-            "workload": (f"C2: Cox PH, Breslow ties, N={args.n}, p={args.p}, "
-                         f"{args.density * 100:g}% binary, L1 gamma=sqrt(2)"),
-            "n": args.n, "p": args.p, "density": args.density, "nnz": int(sim.nnz),
-            "penalty": "l1", "strength": args.strength, "time_quantum": args.quantum,
-            "censoring_quantile": args.censoring_quantile,
-            "step": "one CCD cycle = one persistent cycle-kernel launch (p coordinates + objective)",
-            "l2": "inputs larger than L2: per-cycle working set ~2.5 GB (no flush needed)",
-            "parallelism": f"replicas{dist.world}",
-        },
+        "config": {**c2_config(args, dist.world), "nnz": int(sim.nnz),
+                   "step": "one CCD cycle = one persistent cycle-kernel launch (p coordinates + "
+                           "objective)",
+                   "l2": "inputs larger than L2: per-cycle working set ~2.5 GB (no flush needed)"},
         "e2e": {"value": round(float(np.mean(e2e_vals)), 2) if e2e_vals else None,
                 "unit": "coord_updates/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(args.p * 8),
@@ -670,6 +664,15 @@ def run_c5(args, dist):
                        "shard aggregates per grid exchange"}
 
 
+def c2_config(args, world):
+    """The headline workload's config keys, shared by both arms."""
+    return {"workload": (f"C2: Cox PH, Breslow ties, N={args.n}, p={args.p}, "
+                         f"{args.density * 100:g}% binary, L1 gamma=sqrt(2)"),
+            "n": args.n, "p": args.p, "density": args.density, "penalty": "l1",
+            "strength": args.strength, "time_quantum": args.quantum,
+            "censoring_quantile": args.censoring_quantile, "parallelism": f"replicas{world}"}
+
+
 def main():
     args = parse()
     dist = Dist(args.gpus)
@@ -680,8 +683,10 @@ def main():
                     "unit": "coord_updates/s", "impl": "reference", "n_gpus": dist.world,
                     "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                     "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                    "config": {"workload": "C2 sample for the CPU reference", "n": args.n,
-                               "p_sample": args.cpu_sample_p, "density": args.density},
+                    # the arm's config (same workload keys as the gss line); the
+                    # bounded sample actually timed is cpu_baseline.sample
+                    "config": {**c2_config(args, dist.world),
+                               "reference_sample_columns": args.cpu_sample_p},
                     "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind",
                                                        "sample")},
                     "e2e": {"value": round(r["value"], 3), "unit": "coord_updates/s",
