@@ -197,6 +197,7 @@ struct gss_engine {
   std::vector<int32_t> h_slots;   // slots of the staged CCD cycle
   // device
   double *eta = nullptr, *e = nullptr, *scratch = nullptr, *g = nullptr;
+  double* gs = nullptr;  // streamed G: u = 1/G on competing rows without events (Fine-Gray)
   uint32_t* code = nullptr;
   double *beta = nullptr, *halfwidth = nullptr, *fixed = nullptr;
   uint8_t* penalized = nullptr;
@@ -236,7 +237,7 @@ struct gss_engine {
     cudaSetDevice(ds->device);
     if (stream) cudaStreamSynchronize(stream);
     // pool allocations (ealloc): stream-ordered frees, no device-wide sync
-    for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)code, (void*)beta,
+    for (void* q : {(void*)eta, (void*)e, (void*)scratch, (void*)g, (void*)gs, (void*)code, (void*)beta,
                     (void*)halfwidth, (void*)fixed, (void*)penalized, (void*)trec, (void*)tcar,
                     (void*)cpay, (void*)slot_out, (void*)slot_col, (void*)bar, (void*)ctl,
                     (void*)dflag, (void*)ext, (void*)shard, (void*)cta_tile0})
@@ -775,7 +776,10 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(ealloc(&E->ext, 8, E->stream));
   EK(ealloc(&E->shard, 8, E->stream));
   EK(cudaMemsetAsync(E->ext, 0, 8 * sizeof(double), E->stream));
-  if (E->weighted) EK(ealloc(&E->g, npad, E->stream));
+  if (E->weighted) {
+    EK(ealloc(&E->g, npad, E->stream));
+    EK(ealloc(&E->gs, npad, E->stream));
+  }
   EK(cudaMallocHost(reinterpret_cast<void**>(&E->h_ctl), sizeof(Ctl)));
   std::memset(E->h_ctl, 0, sizeof(Ctl));
   E->h_ctl->err_col = -1;
@@ -794,6 +798,14 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
       std::vector<double> gd(static_cast<size_t>(npad), 1.0);
       for (int64_t i = 0; i < n; ++i) gd[ds->dev_row[i]] = E->h_g[i];
       EK(cudaMemcpyAsync(E->g, gd.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
+      // The streamed copy carries u = 1/G on competing rows (the reference's
+      // 1.0 / before, src/censoring.cpp) and G elsewhere, so the scan does not
+      // divide per row; the Breslow transform needs G at tied-block ends and
+      // divides back there when the block-end row is competing.
+      std::vector<double> gsd(gd);
+      for (int64_t r = 0; r < npad; ++r)
+        if (E->h_code[r] & kCodeCompeting) gsd[r] = 1.0 / gd[r];
+      EK(cudaMemcpyAsync(E->gs, gsd.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
       EK(cudaStreamSynchronize(s));
     } else {
       EK(cudaStreamSynchronize(s));
@@ -810,7 +822,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   rc = make_tile_map(&E->tm_code, E->code, npad, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4);
   if (rc) return bail(rc);
   if (E->weighted) {
-    rc = make_tile_map(&E->tm_g, E->g, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8);
+    rc = make_tile_map(&E->tm_g, E->gs, npad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8);
     if (rc) return bail(rc);
   } else {
     E->tm_g = E->tm_e;

@@ -573,6 +573,15 @@ __device__ __forceinline__ void producer(const CycleParams& P, unsigned char* sm
 // consumer: one tile of one slot, processed by a group of kGW warps
 // (warp gw of the group owns passes [gw*PPW, (gw+1)*PPW) of the tile)
 // ---------------------------------------------------------------------------
+// staged Fine-Gray weight of a row (gss_engine::gs): u = 1/G(Y-) on
+// competing rows, G elsewhere
+__device__ __forceinline__ double u_of(uint32_t code, double staged) {
+  return (code & kCodeCompeting) ? staged : 0.0;
+}
+__device__ __forceinline__ double g_of(uint32_t code, double staged) {
+  return (code & kCodeCompeting) ? __drcp_rn(staged) : staged;
+}
+
 template <int L>
 struct Lanes {
   double v[L];
@@ -747,7 +756,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
         R.gv[2 * c + 1] = v.y;
       }
 #pragma unroll
-      for (int m = 0; m < kIpt; ++m) R.uv[m] = (R.cw[m] & kCodeCompeting) ? __drcp_rn(R.gv[m]) : 0.0;
+      for (int m = 0; m < kIpt; ++m) R.uv[m] = u_of(R.cw[m], R.gv[m]);
     }
     R.xb = 0;
     R.nb = 0;
@@ -927,7 +936,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
         if constexpr (FG) {
           // u-weighted suffix strictly after this row, inside the stratum:
           // S(k+1) = RcarryTot - inclusive in-tile prefix
-          const double gk = R.gv[m];
+          const double gk = g_of(R.cw[m], R.gv[m]);  // G at the block end
           den = __dadd_rn(den, __dmul_rn(gk, __dsub_rn(cr[0], run.v[NF])));
           if constexpr (NF >= 2) {
             n1 = __dadd_rn(n1, __dmul_rn(gk, __dsub_rn(cr[1], run.v[NF + 1])));
@@ -994,7 +1003,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       double u = 0.0;
       if constexpr (FG) {
         if (code_at(sc, lr) & kCodeCompeting)
-          u = __drcp_rn(*reinterpret_cast<const double*>(sg + swz<128>(lr * 8)));
+          u = u_of(code_at(sc, lr), *reinterpret_cast<const double*>(sg + swz<128>(lr * 8)));
         rub = __dadd_rn(rub, __dmul_rn(u, eb));
         ruc = __dadd_rn(ruc, __dmul_rn(u, ec));
       }
@@ -1022,7 +1031,7 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
         if constexpr (FG) {
           if (code_at(sc, lr) & kCodeCompeting)
             rusa = __dadd_rn(
-                rusa, __dmul_rn(__drcp_rn(*reinterpret_cast<const double*>(sg + swz<128>(lr * 8))),
+                rusa, __dmul_rn(u_of(code_at(sc, lr), *reinterpret_cast<const double*>(sg + swz<128>(lr * 8))),
                                 ev));
         }
       }
