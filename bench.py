@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--strength", type=float, default=math.sqrt(2.0))
     ap.add_argument("--quantum", type=float, default=1000.0)
     ap.add_argument("--censoring-quantile", type=float, default=0.9)
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-max-cycles", type=int, default=60)
     ap.add_argument("--cpu-sample-p", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
