@@ -208,6 +208,46 @@ def test_finegray_multitile_vs_oracle(capi, n, p, quant, strata, valued):
     assert np.max(rel(r1["objective_trace"], r2["objective_trace"])) < TOL_DERIV
 
 
+def test_finegray_competing_block_ends_vs_oracle(capi):
+    """Tied blocks with events whose last row (the Breslow transform's row) is a
+    competing row, with censoring before them (G < 1): the kernel streams
+    u = 1/G on competing rows and recovers G at those block ends."""
+    rng = np.random.default_rng(29)
+    n, p = 80_000, 8
+    t = np.ceil(rng.exponential(size=n) * 40.0) / 40.0
+    status = np.where(rng.random(n) < 0.5, 1, np.where(rng.random(n) < 0.5, 2, 0))
+    # sorted order is (time desc, row id asc): a block's last row has the largest id
+    last = {}
+    for i in range(n):
+        last[t[i]] = i
+    has_event = {}
+    for i in range(n):
+        if status[i] == 1:
+            has_event[t[i]] = True
+    ends = [i for tv, i in last.items() if has_event.get(tv)]
+    status[ends] = 2
+    assert len(ends) > 100
+    per = [rng.choice(n, size=rng.binomial(n, 0.04), replace=False) for _ in range(p)]
+    rows = np.concatenate(per)
+    cols = np.concatenate([np.full(len(r), j) for j, r in enumerate(per)])
+    ds = orc.assemble(t, status, rows, cols, np.ones(len(rows)), p)
+    ref = orc.OracleEngine(ds, "finegray")
+    eng = capi.Engine(capi.Dataset.from_sorted(ds), "finegray")
+    beta = np.random.default_rng(31).uniform(-0.3, 0.3, size=p)
+    ref.load_beta(beta)
+    eng.load_beta(beta)
+    assert rel(eng.log_likelihood(), ref.log_likelihood()) < TOL_DERIV
+    for j in range(p):
+        a, b = eng.grad_hessian(j), ref.grad_hessian(j)
+        assert rel_cond(a["gradient"], b["gradient"], b["fixed_term"]) < TOL_DERIV, j
+        assert rel(a["hessian"], b["hessian"]) < TOL_DERIV, j
+    r1 = capi.Engine(capi.Dataset.from_sorted(ds), "finegray").fit(penalty="l1", strength=1.0,
+                                                                    max_cycles=4)
+    r2 = orc.OracleEngine(ds, "finegray").fit(penalty="l1", strength=1.0, max_cycles=4)
+    assert r1["cycles"] == r2["cycles"]
+    assert np.max(rel(r1["beta"], r2["beta"])) < TOL_BETA
+
+
 def test_finegray_mask_equals_subset(capi):
     ds = _random_sorted(40_000, 6, 0.05, seed=21, quant=30.0, competing=0.5)
     mask = (np.random.default_rng(2).random(ds.n) < 0.75).astype(np.uint8)
