@@ -436,17 +436,21 @@ int partition_ctas(gss_engine* E, int grid) {
   const int nt = E->ds->ntiles;
   grid = std::max(1, std::min(grid, std::min(nt, E->max_grid)));
   std::vector<double> w(static_cast<size_t>(nt), 1.0);
-  // Per-tile cost model: 1 + 0.12 if any pass holds a transform + 0.04 per
-  // such pass.  A consumer group's tile costs the longest of its warps, so the
-  // first transform pass costs most (tools/tile_cost_probe.py: ~5.8k cycles
-  // without, ~7.9k with); the p = 512 C2-design fit measured 42.3 us per
-  // coordinate with this model vs 43.4 with 1 + 0.05 per pass and 46.0
-  // unweighted (tools/gpu_partition_sweep.sh).  A per-event-block-end term
-  // (GSS_BE_W) made the C2 bench slower at 0.05 / 0.1, so it defaults to 0.
-  static const double kPassW =
-      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : 0.04;
-  static const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
-  static const double kAnyW = std::getenv("GSS_ANY_W") ? std::atof(std::getenv("GSS_ANY_W")) : 0.12;
+  // Per-tile cost model (Cox): 1 + 0.12 if any pass holds a transform + 0.04
+  // per such pass.  A consumer group's tile costs the longest of its warps, so
+  // the first transform pass costs most (tools/tile_cost_probe.py: ~5.8k
+  // cycles without, ~7.9k with); the p = 512 C2-design fit measured 42.3 us
+  // per coordinate with this model vs 43.4 with 1 + 0.05 per pass and 46.0
+  // unweighted (tools/gpu_partition_sweep.sh).  Fine-Gray (8-warp groups, one
+  // pass per warp) is best at 1 + 0.05 per pass: 79.6 vs 82.2 us (p = 512),
+  // 79.2 vs 81.7 (p = 5000).  A per-event-block-end term (GSS_BE_W) made the
+  // C2 bench slower at 0.05 / 0.1, so it defaults to 0.
+  const bool fg_w = E->weighted;
+  const double kPassW =
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : (fg_w ? 0.05 : 0.04);
+  const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
+  const double kAnyW =
+      std::getenv("GSS_ANY_W") ? std::atof(std::getenv("GSS_ANY_W")) : (fg_w ? 0.0 : 0.12);
   for (int t = 0; t < nt; ++t) {
     int work = 0, ends = 0;
     for (int pass = 0; pass < kTileRows / 256; ++pass) {
