@@ -144,7 +144,19 @@ def test_multiprocess_shards_under_mps(world, grid, tmp_path):
             env=env, capture_output=True, text=True, timeout=240, cwd=root)
     finally:
         subprocess.run([ctl], input="quit\n", env=env, text=True)
-    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    # the ranks share one stdout pipe: decode every JSON object in it, even
+    # two that landed on one line
+    dec, lines, i, txt = json.JSONDecoder(), [], 0, out.stdout
+    while True:
+        i = txt.find("{", i)
+        if i < 0:
+            break
+        try:
+            obj, i = dec.raw_decode(txt, i)
+        except json.JSONDecodeError:
+            i += 1
+            continue
+        lines.append(obj)
     assert out.returncode == 0 and len(lines) == world, out.stderr[-2000:]
     assert len({ln["objective"] for ln in lines}) == 1
     r0 = [ln for ln in lines if ln["rank"] == 0][0]

@@ -42,8 +42,10 @@ if a.sim:
     r = sharded.fit_in_kernel_distributed(ds, penalty="l1", strength=2 ** 0.5, tol=1e-300,
                                           max_cycles=3, device=dev, grid=a.grid)
     us = r["device_seconds"] / (r["cycles"] * (a.p + 1)) * 1e6
-    print(json.dumps({"rank": rank, "world": world, "rows_total": a.sim, "p": a.p, "grid": a.grid,
-                      "us_per_coordinate": round(us, 2), "objective": r["objective"]}), flush=True)
+    sys.stdout.write(json.dumps({"rank": rank, "world": world, "rows_total": a.sim, "p": a.p,
+                                 "grid": a.grid, "us_per_coordinate": round(us, 2),
+                                 "objective": r["objective"]}) + "\n")
+    sys.stdout.flush()
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0)
@@ -57,6 +59,8 @@ if rank == 0:
     err = float(np.max(np.abs(r["beta"] - one["beta"]) / np.maximum(1.0, np.abs(one["beta"]))))
     out.update({"unsharded_cycles": one["cycles"], "max_rel_err_beta": err,
                 "pass": bool(err < 1e-8 and one["cycles"] == r["cycles"])})
-print(json.dumps(out), flush=True)
+# one write per line: ranks share the launcher's stdout pipe
+sys.stdout.write(json.dumps(out) + "\n")
+sys.stdout.flush()
 dist.barrier()
 dist.destroy_process_group()
