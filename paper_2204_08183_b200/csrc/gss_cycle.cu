@@ -430,8 +430,10 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
   if (mbar_try_wait(bar, parity)) return;
   const unsigned long long t0 = gtimer();
   unsigned it = 0;
+  // try_wait suspends the warp in hardware until the phase completes or a
+  // time limit passes, so the retry needs no software back-off (measured:
+  // a 64 ns sleep here cost 0.4% per coordinate)
   while (!mbar_try_wait(bar, parity)) {
-    __nanosleep(64);  // back off: spinning waiters would steal the producer's issue slots
     if ((++it & 63u) == 0 && gtimer() - t0 > kWatchdogNs) watchdog_trap(what, info, parity, marks);
   }
 }
