@@ -31,8 +31,11 @@ m = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 def num(key, scale=1.0):
     v, u = m[key]
     v = float(v.replace(",", ""))
-    mult = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6,
-            "ns": 1e-9, "s": 1.0}.get(u, 1.0)
+    mult = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3,
+            "us": 1e-6, "ns": 1e-9, "s": 1.0, "%": 1.0, "register/thread": 1.0}.get(u)
+    if mult is None and u and ("byte" in u or u.endswith("s")):
+        raise ValueError(f"unknown unit {u!r} for {key}")
+    mult = mult or 1.0
     return v * mult * scale
 
 
