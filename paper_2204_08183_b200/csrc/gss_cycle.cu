@@ -1047,8 +1047,16 @@ __device__ __forceinline__ void process_tile(const CycleParams& P, Tail<FG>* tl,
       rv[8] = rusb;
       rv[9] = rusc;
     }
+    // Fine-Gray (8-warp groups, 10 partials): warps past both slices summed
+    // nothing (their partials are +0.0 exactly), so they skip the shuffles
+    // (warp-uniform).  Cox keeps the unconditional form: the branch changed
+    // the whole kernel's register allocation and cost 7% on the fused path.
+    const bool warp_had =
+        !FG || gw * 32 < nlim || (ccd_cur && gw * 32 < (dcur ? kTileRows : Lc.cnt));
+    if (warp_had) {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) rv[i] = warp_sum(rv[i]);
+      for (int i = 0; i < NR; ++i) rv[i] = warp_sum(rv[i]);
+    }
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < NR; ++i) tl->gr[g][gw][i] = rv[i];
