@@ -1410,16 +1410,22 @@ int gss_fit_batch(gss_engine* const* engines, int64_t count, const gss_penalty_s
       if (engines[i]->weighted == weighted) queue.push_back(i);
     if (queue.empty()) continue;
     const int maxg = engines[queue[0]]->max_grid;
-    int slots = max_active > 0 ? max_active : kMaxBatch;
+    // fits per launch at the default concurrency (a process-wide constant, so
+    // every fit's CTA share is the same in every call)
+    static const int kBatchW = [] {
+      const char* b = std::getenv("GSS_BATCH_MAX");
+      return b ? std::max(1, std::min(kMaxBatch, std::atoi(b))) : kMaxBatch;
+    }();
+    int slots = max_active > 0 ? max_active : kBatchW;
     if (max_active <= 0)
       if (const char* a = std::getenv("GSS_BATCH_ACTIVE")) slots = std::max(1, std::atoi(a));
-    slots = std::max(1, std::min({slots, kMaxBatch, maxg, static_cast<int>(queue.size())}));
+    slots = std::max(1, std::min({slots, kBatchW, maxg, static_cast<int>(queue.size())}));
     // CTAs per fit: with the default concurrency every fit gets maxg / kMaxBatch
     // CTAs whatever the batch holds, so a fit's CTA partition (hence its
     // summation order) never depends on how many fits share its launch: CV and
     // bootstrap results are bit-identical across worker and device counts (the
     // reference's guarantee, tests/acceptance.cpp:346-383)
-    const int share = std::max(1, maxg / (max_active > 0 ? slots : kMaxBatch));
+    const int share = std::max(1, maxg / (max_active > 0 ? slots : kBatchW));
     size_t next = 0;
     std::vector<int64_t> active;
     auto finish = [&](int64_t i, int rc) {
