@@ -447,10 +447,10 @@ int partition_ctas(gss_engine* E, int grid) {
   // C2 bench slower at 0.05 / 0.1, so it defaults to 0.
   const bool fg_w = E->weighted;
   const double kPassW =
-      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : (fg_w ? 0.05 : 0.04);
-  const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : 0.0;
+      std::getenv("GSS_PASS_W") ? std::atof(std::getenv("GSS_PASS_W")) : (fg_w ? 0.05 : 0.028);
+  const double kBeW = std::getenv("GSS_BE_W") ? std::atof(std::getenv("GSS_BE_W")) : (fg_w ? 0.0 : 0.0023);
   const double kAnyW =
-      std::getenv("GSS_ANY_W") ? std::atof(std::getenv("GSS_ANY_W")) : (fg_w ? 0.0 : 0.12);
+      std::getenv("GSS_ANY_W") ? std::atof(std::getenv("GSS_ANY_W")) : (fg_w ? 0.0 : 0.15);
   for (int t = 0; t < nt; ++t) {
     int work = 0, ends = 0;
     for (int pass = 0; pass < kTileRows / 256; ++pass) {
@@ -462,6 +462,21 @@ int partition_ctas(gss_engine* E, int grid) {
     }
     // (distinct event times saturate at one transform per row: cap at 4)
     w[t] = std::min(4.0, 1.0 + kPassW * work + kBeW * double(ends) + (work ? kAnyW : 0.0));
+    if (std::getenv("GSS_TILE_DUMP")) {  // per-tile features for the cost-model fit
+      int ev = 0, wmax = 0;
+      for (int r = 0; r < kTileRows; ++r) ev += (E->h_code[size_t(t) * kTileRows + r] & kCodeEvent) != 0;
+      for (int gw = 0; gw < 4; ++gw) {
+        int c = 0;
+        for (int pp = 2 * gw; pp < 2 * gw + 2; ++pp) {
+          int a = 0;
+          for (int r = 0; r < 256; ++r)
+            a |= (E->h_code[size_t(t) * kTileRows + pp * 256 + r] & kCodeCount) != 0;
+          c += a;
+        }
+        wmax = std::max(wmax, c);
+      }
+      std::fprintf(stderr, "tile %d work %d ends %d events %d wmax %d\n", t, work, ends, ev, wmax);
+    }
   }
   double tot = 0.0;
   for (double x : w) tot += x;
