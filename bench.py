@@ -461,17 +461,20 @@ def run_gss(args, dist):
         parity = parity_spot_check(sim, eng)
     del eng
     # ---------------- end-to-end through the C ABI from host buffers -----
-    e2e_vals, ttf, e2e_cycles = [], [], []
+    e2e_vals, ttf, e2e_cycles, phases = [], [], [], []
     h2d = int(sim.host_bytes())
     for _ in range(args.e2e_steps):
         dist.barrier()
         t0 = time.perf_counter()
         d2 = capi.Dataset(sim.times, sim.status, sim.col_ptr, sim.row_idx, device=dev)
+        t1 = time.perf_counter()
         e2 = capi.Engine(d2, "cox")
+        t2 = time.perf_counter()
         r2 = e2.fit(penalty="l1", strength=args.strength, tol=1e-6,
                     max_cycles=args.e2e_max_cycles)
         beta = r2["beta"]  # device -> host read of the result
         wall = time.perf_counter() - t0
+        phases.append((t1 - t0, t2 - t1, t0 + wall - t2))
         wall = dist.max(wall)
         e2e_vals.append(dist.sum(r2["cycles"] * args.p) / wall)
         ttf.append(wall)
@@ -509,6 +512,7 @@ def run_gss(args, dist):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(args.p * 8),
                 "time_to_fit_s": round(float(np.mean(ttf)), 3) if ttf else None,
                 "cycles_to_converge": e2e_cycles,
+                "phase_seconds_mean": {k: round(float(np.mean([ph[i] for ph in phases])), 3) for i, k in enumerate(("pack", "engine_create", "fit"))} if phases else None,
                 "path": "gss_dataset_pack + gss_engine_create + gss_engine_fit (tol 1e-6) from "
                         "pinned host buffers"},
         "roofline": roof,

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -77,6 +78,43 @@ namespace {
       return fail(_e == cudaErrorMemoryAllocation ? GSS_ERR_OOM : GSS_ERR_CUDA,         \
                   std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #call); \
   } while (0)
+
+// Host vectors whose resize() leaves elements uninitialised, so the pages of
+// a 10M-row copy are first touched by the parallel fill below, not serially.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  DefaultInitAlloc() = default;
+  template <class U>
+  DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* q) noexcept {
+    ::new (static_cast<void*>(q)) U;
+  }
+  template <class U, class... A>
+  void construct(U* q, A&&... a) {
+    ::new (static_cast<void*>(q)) U(std::forward<A>(a)...);
+  }
+};
+
+// f(lo, hi) over [0, n) in contiguous chunks on up to 16 host threads
+// (chunk c covers [n*c/T, n*(c+1)/T)); serial below 1M rows.
+template <class F>
+void host_parallel(int64_t n, F&& f) {
+  const unsigned hc = std::thread::hardware_concurrency();
+  const int T = n < (int64_t(1) << 20) ? 1 : static_cast<int>(std::min(16u, std::max(1u, hc)));
+  if (T == 1) {
+    f(0, 0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (int c = 0; c < T; ++c) th.emplace_back([&f, c, n, T]() { f(c, n * c / T, n * (c + 1) / T); });
+  for (auto& t : th) t.join();
+}
 
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -149,10 +187,13 @@ struct gss_dataset {
   int ntiles = 0;
   bool has_vals = false;
   // host copies needed per engine (row codes, IPCW) — sorted order
-  std::vector<double> times;
-  std::vector<int32_t> status;
-  std::vector<int64_t> stratum_of;   // stratum ordinal per sorted row
-  std::vector<int64_t> dev_row;      // sorted row -> device position
+  template <class T>
+  using hvec = std::vector<T, DefaultInitAlloc<T>>;
+  hvec<double> times;
+  hvec<int32_t> status;
+  hvec<int64_t> stratum_of;   // stratum ordinal per sorted row
+  hvec<int64_t> dev_row;      // sorted row -> device position
+  bool identity_rows = false;  // dev_row[i] == i (no stratum padding)
   std::vector<uint8_t> h_tile_first;
   // device
   int64_t* col_ptr = nullptr;
@@ -168,8 +209,10 @@ struct gss_dataset {
   int32_t* dense_idx = nullptr;      // [p] dense-pool slot or -1 (density >= 25%)
   double* dense_pool = nullptr;      // [ndense][npad]
   int64_t ndense = 0;
-  int64_t bytes = 0;
+  int64_t bytes = 0;  // footprint including the CSR built on the first load_beta
   std::vector<int64_t> h_col_ptr;
+  std::mutex csr_mu;
+  bool csr_built = false;
 
   ~gss_dataset() {
     int prev = -1;
@@ -541,14 +584,43 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   GSS_CUDA(cudaSetDevice(device));
   const int64_t n = h->n, p = h->p;
   const int64_t nnz = p > 0 ? h->col_ptr[p] : 0;
-  // validate the layout contract (sorted rows, ascending CSC indices)
-  for (int64_t i = 0; i < n; ++i) {
-    if (!std::isfinite(h->times[i]) || h->times[i] < 0.0)
-      return fail(GSS_ERR_DOMAIN, "observation time must be finite and >= 0");
-    if (h->status[i] < 0 || h->status[i] > 2) return fail(GSS_ERR_DOMAIN, "status must be 0, 1 or 2");
-    const bool new_stratum = h->stratum_start && h->stratum_start[i];
-    if (i > 0 && !new_stratum && h->times[i] > h->times[i - 1])
+  // GSS_PACK_TIMING: per-phase wall times (stream synchronised at each mark)
+  const bool ptime = std::getenv("GSS_PACK_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  cudaStream_t* ps = nullptr;
+  auto mark = [&](const char* what) {
+    if (!ptime) return;
+    if (ps) cudaStreamSynchronize(*ps);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "pack %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
+  // validate the layout contract (sorted rows, ascending CSC indices); the
+  // first failing row decides the message, as in a serial pass
+  {
+    std::vector<int64_t> bad_row(16, -1);
+    std::vector<int> bad_code(16, 0);
+    host_parallel(n, [&](int c, int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        int code = 0;
+        if (!std::isfinite(h->times[i]) || h->times[i] < 0.0) code = 1;
+        else if (h->status[i] < 0 || h->status[i] > 2) code = 2;
+        else if (i > 0 && !(h->stratum_start && h->stratum_start[i]) && h->times[i] > h->times[i - 1])
+          code = 3;
+        if (code) {
+          bad_row[c] = i;
+          bad_code[c] = code;
+          return;
+        }
+      }
+    });
+    for (int c = 0; c < 16; ++c) {
+      if (bad_row[c] < 0) continue;
+      if (bad_code[c] == 1) return fail(GSS_ERR_DOMAIN, "observation time must be finite and >= 0");
+      if (bad_code[c] == 2) return fail(GSS_ERR_DOMAIN, "status must be 0, 1 or 2");
       return fail(GSS_ERR_DOMAIN, "rows must be sorted by decreasing time within a stratum");
+    }
   }
   if (p > 0 && h->col_ptr[0] != 0) return fail(GSS_ERR_DOMAIN, "col_ptr[0] must be 0");
   auto* ds = new gss_dataset();
@@ -556,21 +628,40 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   ds->n = n;
   ds->p = p;
   ds->nnz = nnz;
-  ds->times.assign(h->times, h->times + n);
-  ds->status.assign(h->status, h->status + n);
+  ds->times.resize(static_cast<size_t>(n));
+  ds->status.resize(static_cast<size_t>(n));
   // stratum-aligned device layout
   ds->stratum_of.resize(static_cast<size_t>(n));
   ds->dev_row.resize(static_cast<size_t>(n));
   {
-    int64_t stratum = -1, pos = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      if (i == 0 || (h->stratum_start && h->stratum_start[i])) {
-        ++stratum;
-        pos = (pos + kTileRows - 1) / kTileRows * kTileRows;  // next tile boundary
+    int64_t pos = 0;
+    if (!h->stratum_start) {  // one stratum: device position = sorted row
+      host_parallel(n, [&](int, int64_t lo, int64_t hi) {
+        std::memcpy(ds->times.data() + lo, h->times + lo, (hi - lo) * sizeof(double));
+        std::memcpy(ds->status.data() + lo, h->status + lo, (hi - lo) * sizeof(int32_t));
+        for (int64_t i = lo; i < hi; ++i) {
+          ds->stratum_of[i] = 0;
+          ds->dev_row[i] = i;
+        }
+      });
+      pos = n;
+    } else {
+      host_parallel(n, [&](int, int64_t lo, int64_t hi) {
+        std::memcpy(ds->times.data() + lo, h->times + lo, (hi - lo) * sizeof(double));
+        std::memcpy(ds->status.data() + lo, h->status + lo, (hi - lo) * sizeof(int32_t));
+      });
+      int64_t stratum = -1;
+      for (int64_t i = 0; i < n; ++i) {
+        if (i == 0 || h->stratum_start[i]) {
+          ++stratum;
+          pos = (pos + kTileRows - 1) / kTileRows * kTileRows;  // next tile boundary
+        }
+        ds->stratum_of[i] = stratum;
+        ds->dev_row[i] = pos++;
       }
-      ds->stratum_of[i] = stratum;
-      ds->dev_row[i] = pos++;
     }
+    // positions rise by >= 1 per row, so the map is the identity iff the last row is
+    ds->identity_rows = n == 0 || ds->dev_row[n - 1] == n - 1;
     int64_t npad = (pos + kTileRows - 1) / kTileRows * kTileRows;
     if (npad == 0) npad = kTileRows;
     if (npad >= (int64_t(1) << 31) - kTileRows) {
@@ -587,9 +678,10 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     // row 0 starts a stratum unless the caller marks it as continuing one from
     // a previous patient shard (stratum_start[0] == 0)
     ds->h_tile_first[0] = (h->stratum_start && n > 0) ? (h->stratum_start[0] ? 1 : 0) : 1;
-    for (int64_t i = 1; i < n; ++i)
-      if (ds->stratum_of[i] != ds->stratum_of[i - 1])
-        ds->h_tile_first[ds->dev_row[i] / kTileRows] = 1;
+    if (h->stratum_start)
+      for (int64_t i = 1; i < n; ++i)
+        if (ds->stratum_of[i] != ds->stratum_of[i - 1])
+          ds->h_tile_first[ds->dev_row[i] / kTileRows] = 1;
   }
   ds->h_col_ptr.assign(h->col_ptr, h->col_ptr + p + 1);
   if (p == 0) ds->h_col_ptr.assign(1, 0);
@@ -609,8 +701,10 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     if (!ind[j]) any_valued = true;
   }
   ds->has_vals = h->vals != nullptr && any_valued;
+  mark("host layout");
   cudaStream_t s;
   GSS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  ps = &s;
   auto cleanup = [&](int rc) {
     cudaStreamDestroy(s);
     if (rc != GSS_OK) delete ds;
@@ -628,16 +722,14 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   PK(dalloc(&ds->row_idx, nnz + 4));
   PK(dalloc(&ds->col_ind, p));
   PK(dalloc(&ds->tile_ptr, p * (ds->ntiles + 1)));
-  PK(dalloc(&ds->row_ptr, npad + 1));
-  PK(dalloc(&ds->csr_col, nnz + 4));
   PK(dalloc(&ds->colmax, p));
   PK(dalloc(&ds->tile_first, ds->ntiles));
   if (ds->has_vals) {
     PK(dalloc(&ds->vals, nnz + 4));
-    PK(dalloc(&ds->csr_val, nnz + 4));
   }
   ds->bytes = (p + 1) * 8 + (nnz + 4) * 8 + p + int64_t(p) * (ds->ntiles + 1) * 4 +
               (npad + 1) * 8 + p * 8 + ds->ntiles + (ds->has_vals ? (nnz + 4) * 16 : 0);
+  mark("alloc");
   PK(cudaMemcpyAsync(ds->col_ptr, ds->h_col_ptr.data(), (p + 1) * sizeof(int64_t),
                      cudaMemcpyHostToDevice, s));
   PK(cudaMemsetAsync(ds->row_idx, 0, (nnz + 4) * sizeof(int32_t), s));
@@ -648,6 +740,7 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     PK(cudaMemcpyAsync(ds->vals, h->vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
   PK(cudaMemcpyAsync(ds->tile_first, ds->h_tile_first.data(), ds->ntiles, cudaMemcpyHostToDevice,
                      s));
+  mark("h2d");
   {
     Nvtx nv("pack: validate csc");
     int* bad = nullptr;
@@ -662,7 +755,8 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     if (hb) return cleanup(fail(GSS_ERR_DOMAIN, "CSC columns must have monotone col_ptr and "
                                                 "strictly ascending row indices"));
   }
-  if (npad != n) {  // remap to the stratum-aligned positions (order preserving)
+  mark("validate csc");
+  if (!ds->identity_rows) {  // remap to the stratum-aligned positions (order preserving)
     int64_t* drow = nullptr;
     PK(dalloc(&drow, std::max<int64_t>(n, 1)));
     if (n)
@@ -671,6 +765,7 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     PK(cudaStreamSynchronize(s));
     cudaFree(drow);
   }
+  mark("remap");
   if (p) {
     Nvtx nv("pack: tile pointers + colmax");
     PK(launch_build_tile_ptr(ds->col_ptr, ds->row_idx, p, ds->ntiles, ds->tile_ptr, s));
@@ -679,6 +774,7 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
   // Dense columns (density >= 25%: the reference stores them as dense arrays,
   // SparseColumn::make src/dataset.cpp:126-157): values by device position in
   // a pool the cycle kernel reads row-wise instead of their tile index lists.
+  mark("tile ptr + colmax");
   if (p) {
     Nvtx nv("pack: dense columns");
     std::vector<int32_t> slot(static_cast<size_t>(p), -1);
@@ -697,25 +793,49 @@ int gss_dataset_pack(const gss_host_dataset* h, int device, gss_dataset** out) {
     }
     ds->bytes += p * 4;
   }
-  // CSR transpose over device positions: count -> exclusive scan -> fill -> per-row sort
-  {
-    Nvtx nv("pack: csr transpose");
-    int64_t* cnt = nullptr;
-    PK(dalloc(&cnt, npad + 1));
-    PK(cudaMemsetAsync(cnt, 0, (npad + 1) * sizeof(int64_t), s));
-    PK(launch_csr_count(ds->row_idx, nnz, cnt, s));
-    PK(launch_exclusive_scan(cnt, ds->row_ptr, npad + 1, s));
-    PK(cudaMemcpyAsync(cnt, ds->row_ptr, (npad + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-    PK(launch_csr_fill(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, p, cnt,
-                       ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
-    PK(launch_csr_sort_rows(ds->row_ptr, npad, ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, s));
-    PK(cudaStreamSynchronize(s));
-    cudaFree(cnt);
-  }
+  mark("dense");
 #undef PK
   *out = ds;
   return cleanup(GSS_OK);
 }
+
+namespace {
+// CSR transpose over device positions (count -> exclusive scan -> fill ->
+// per-row sort), built on the first load_beta: the row-wise η = Xβ is its only
+// reader, so a fit from β = 0 never pays for it.
+int ensure_csr(gss_dataset* ds) {
+  std::lock_guard<std::mutex> lk(ds->csr_mu);
+  if (ds->csr_built) return GSS_OK;
+  Nvtx nv("csr transpose");
+  GSS_CUDA(cudaSetDevice(ds->device));
+  const int64_t npad = ds->npad, nnz = ds->nnz, p = ds->p;
+  struct Res {
+    cudaStream_t s = nullptr;
+    int64_t* cnt = nullptr;
+    ~Res() {
+      if (cnt) cudaFree(cnt);
+      if (s) cudaStreamDestroy(s);
+    }
+  } r;
+  GSS_CUDA(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
+  if (!ds->row_ptr) GSS_CUDA(dalloc(&ds->row_ptr, npad + 1));
+  if (!ds->csr_col) GSS_CUDA(dalloc(&ds->csr_col, nnz + 4));
+  if (ds->has_vals && !ds->csr_val) GSS_CUDA(dalloc(&ds->csr_val, nnz + 4));
+  GSS_CUDA(dalloc(&r.cnt, npad + 1));
+  GSS_CUDA(cudaMemsetAsync(r.cnt, 0, (npad + 1) * sizeof(int64_t), r.s));
+  GSS_CUDA(launch_csr_count(ds->row_idx, nnz, r.cnt, r.s));
+  GSS_CUDA(launch_exclusive_scan(r.cnt, ds->row_ptr, npad + 1, r.s));
+  GSS_CUDA(cudaMemcpyAsync(r.cnt, ds->row_ptr, (npad + 1) * sizeof(int64_t),
+                           cudaMemcpyDeviceToDevice, r.s));
+  GSS_CUDA(launch_csr_fill(ds->col_ptr, ds->row_idx, ds->has_vals ? ds->vals : nullptr, p, r.cnt,
+                           ds->csr_col, ds->has_vals ? ds->csr_val : nullptr, r.s));
+  GSS_CUDA(launch_csr_sort_rows(ds->row_ptr, npad, ds->csr_col,
+                                ds->has_vals ? ds->csr_val : nullptr, r.s));
+  GSS_CUDA(cudaStreamSynchronize(r.s));
+  ds->csr_built = true;
+  return GSS_OK;
+}
+}  // namespace
 
 void gss_dataset_release(gss_dataset* ds) {
   if (ds && --ds->refs == 0) delete ds;
@@ -940,6 +1060,17 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
       cudaFree(dbeta);
       return rc2;
     }
+  }
+  {
+    const int rc2 = ensure_csr(E->ds);
+    if (rc2) {
+      cudaFree(dbeta);
+      return rc2;
+    }
+    GSS_CUDA(cudaSetDevice(E->ds->device));
+    E->prm.row_ptr = E->ds->row_ptr;
+    E->prm.csr_col = E->ds->csr_col;
+    E->prm.csr_val = E->ds->csr_val;
   }
   GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
   GSS_CUDA(launch_spmv_rows(E->prm, dbeta, E->scratch, E->dflag, s));
