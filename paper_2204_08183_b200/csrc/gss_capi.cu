@@ -524,20 +524,73 @@ int partition_ctas(gss_engine* E, int grid) {
   double tot = 0.0;
   for (double x : w) tot += x;
   std::vector<int32_t> t0(static_cast<size_t>(grid) + 1, 0);
-  double acc = 0.0;
-  int c = 1;
-  for (int t = 0; t < nt && c < grid; ++t) {
-    acc += w[t];
-    // cut after tile t once CTA c-1 holds its share (every CTA keeps >= 1 tile)
-    while (c < grid && acc >= tot * c / grid && t + 1 <= nt - (grid - c)) {
-      t0[c] = t + 1;
-      ++c;
+  static const bool greedy = std::getenv("GSS_PART_GREEDY") != nullptr;
+  if (!greedy && nt > grid) {
+    // Min-max contiguous partition: the smallest bound B (bisected in
+    // [tot/grid, tot/grid + max w], where greedy filling needs <= grid ranges)
+    // under which greedy filling fits the grid, then the heaviest multi-tile
+    // ranges are halved until there are exactly `grid`.  A share-crossing cut
+    // leaves a CTA up to one whole tile above the mean; this bounds the
+    // heaviest CTA by the optimum instead.
+    double wmax = 0.0;
+    for (double x : w) wmax = std::max(wmax, x);
+    auto fill = [&](double B, std::vector<int32_t>* cuts) {
+      int cnt = 1;
+      double a = 0.0;
+      if (cuts) cuts->assign(1, 0);
+      for (int t = 0; t < nt; ++t) {
+        if (a > 0.0 && a + w[t] > B) {
+          ++cnt;
+          a = 0.0;
+          if (cuts) cuts->push_back(t);
+        }
+        a += w[t];
+      }
+      if (cuts) cuts->push_back(nt);
+      return cnt;
+    };
+    double lo = tot / grid, hi = tot / grid + wmax;
+    for (int it = 0; it < 60; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      (fill(mid, nullptr) <= grid ? hi : lo) = mid;
     }
+    std::vector<int32_t> cuts;
+    fill(hi, &cuts);
+    while (static_cast<int>(cuts.size()) - 1 < grid) {
+      int best = -1;
+      double bw = -1.0;
+      for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+        if (cuts[k + 1] - cuts[k] < 2) continue;
+        double wk = 0.0;
+        for (int t = cuts[k]; t < cuts[k + 1]; ++t) wk += w[t];
+        if (wk > bw) bw = wk, best = static_cast<int>(k);
+      }
+      double a = 0.0;
+      int m = cuts[best] + 1;
+      for (int t = cuts[best]; t < cuts[best + 1] - 1; ++t) {
+        a += w[t];
+        m = t + 1;
+        if (a >= 0.5 * bw) break;
+      }
+      cuts.insert(cuts.begin() + best + 1, m);
+    }
+    t0.assign(cuts.begin(), cuts.end());
+  } else {
+    double acc = 0.0;
+    int c = 1;
+    for (int t = 0; t < nt && c < grid; ++t) {
+      acc += w[t];
+      // cut after tile t once CTA c-1 holds its share (every CTA keeps >= 1 tile)
+      while (c < grid && acc >= tot * c / grid && t + 1 <= nt - (grid - c)) {
+        t0[c] = t + 1;
+        ++c;
+      }
+    }
+    for (; c < grid; ++c) t0[c] = std::max(t0[c - 1] + 1, nt - (grid - c));
+    t0[grid] = nt;
+    for (int k = 1; k <= grid; ++k)
+      if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
   }
-  for (; c < grid; ++c) t0[c] = std::max(t0[c - 1] + 1, nt - (grid - c));
-  t0[grid] = nt;
-  for (int k = 1; k <= grid; ++k)
-    if (t0[k] <= t0[k - 1]) t0[k] = t0[k - 1] + 1;  // never empty
   if (std::getenv("GSS_VERBOSE")) {
     for (int k = 0; k < grid; ++k) {
       double wk = 0.0;
