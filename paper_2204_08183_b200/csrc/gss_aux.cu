@@ -47,6 +47,14 @@ __global__ void remap_rows_kernel(int32_t* __restrict__ row_idx, int64_t nnz,
 }
 
 // warp per column
+// e = exp(0) on visible rows, 0 on masked rows and padding (engine start)
+__global__ void init_e_kernel(const uint32_t* __restrict__ code, int64_t npad,
+                              double* __restrict__ e) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npad;
+       i += int64_t(gridDim.x) * blockDim.x)
+    e[i] = (code[i] & kCodeMasked) ? 0.0 : 1.0;
+}
+
 __global__ void colmax_kernel(const int64_t* __restrict__ col_ptr, const double* __restrict__ vals,
                               int64_t p, double* __restrict__ colmax) {
   const int lane = threadIdx.x & 31;
@@ -281,6 +289,11 @@ cudaError_t launch_fill_dense(const int64_t* col_ptr, const int32_t* row_idx, co
   if (p == 0) return cudaSuccess;
   fill_dense_kernel<<<grid_for(p * 32, 256), 256, 0, s>>>(col_ptr, row_idx, vals, slot, p, npad,
                                                           pool);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_e(const uint32_t* code, int64_t npad, double* e, cudaStream_t s) {
+  init_e_kernel<<<grid_for(npad, 256), 256, 0, s>>>(code, npad, e);
   return cudaGetLastError();
 }
 

@@ -342,18 +342,29 @@ int device_error(gss_engine* E, const char* where) {
 int build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t>& code) {
   const int64_t n = ds->n;
   code.assign(static_cast<size_t>(ds->npad), kCodeMasked);
-  int64_t s = 0;
-  while (s < n) {
-    int64_t e = s + 1;
-    while (e < n && ds->stratum_of[e] == ds->stratum_of[s]) ++e;
+  // Chunks start at a stratum start or a time change, so no tied block spans
+  // two chunks and each chunk is processed exactly as the serial walk would.
+  std::vector<int> err(16, 0);
+  auto starts_block = [&](int64_t i) {
+    return i == 0 || i >= n || ds->stratum_of[i] != ds->stratum_of[i - 1] ||
+           ds->times[i] != ds->times[i - 1];
+  };
+  host_parallel(n, [&](int ch, int64_t lo, int64_t hi) {
+    while (!starts_block(lo)) ++lo;
+    while (!starts_block(hi)) ++hi;
     int64_t last_vis = -1;
     double last_t = 0.0;
     uint32_t cnt = 0;
-    for (int64_t i = s; i < e; ++i) {
+    for (int64_t i = lo; i < hi; ++i) {
+      const bool seg = i == 0 || ds->stratum_of[i] != ds->stratum_of[i - 1];
+      if (seg) {  // a new stratum closes the previous one's last block
+        if (last_vis >= 0) code[ds->dev_row[last_vis]] |= cnt;
+        last_vis = -1;
+        cnt = 0;
+      }
       uint32_t& c = code[ds->dev_row[i]];
-      c = (i == s) ? kCodeSeg : 0u;
-      const bool vis = !mask || mask[i];
-      if (!vis) {
+      c = seg ? kCodeSeg : 0u;
+      if (mask && !mask[i]) {
         c |= kCodeMasked;
         continue;
       }
@@ -362,7 +373,10 @@ int build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t
         cnt = 0;
       }
       if (ds->status[i] == 1) {
-        if (++cnt > kCodeCount) return fail(GSS_ERR_DOMAIN, "tied block exceeds 2^28 events");
+        if (++cnt > kCodeCount) {
+          err[ch] = 1;
+          return;
+        }
         c |= kCodeEvent;
       } else if (ds->status[i] == 2) {
         c |= kCodeCompeting;
@@ -371,8 +385,9 @@ int build_codes(const gss_dataset* ds, const uint8_t* mask, std::vector<uint32_t
       last_t = ds->times[i];
     }
     if (last_vis >= 0) code[ds->dev_row[last_vis]] |= cnt;
-    s = e;
-  }
+  });
+  for (int e : err)
+    if (e) return fail(GSS_ERR_DOMAIN, "tied block exceeds 2^28 events");
   return GSS_OK;
 }
 
@@ -983,9 +998,7 @@ int gss_engine_create(gss_dataset* ds, int model, int64_t recompute_interval,
   EK(cudaMemcpyAsync(E->code, E->h_code.data(), npad * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   EK(cudaMemsetAsync(E->eta, 0, npad * sizeof(double), s));
   {
-    std::vector<double> e0(static_cast<size_t>(npad), 0.0);
-    for (int64_t i = 0; i < npad; ++i) e0[i] = (E->h_code[i] & kCodeMasked) ? 0.0 : 1.0;
-    EK(cudaMemcpyAsync(E->e, e0.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s));
+    EK(launch_init_e(E->code, npad, E->e, s));
     if (E->weighted) {
       std::vector<double> gd(static_cast<size_t>(npad), 1.0);
       for (int64_t i = 0; i < n; ++i) gd[ds->dev_row[i]] = E->h_g[i];
@@ -1114,7 +1127,16 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
       return rc2;
     }
   }
-  {
+  // beta = 0 on indicator data (every fit's start, ccd.cpp:137): the row sums
+  // are +0.0 + 0 * 1.0 + ... = +0.0 exactly, so eta is a memset and the CSR is
+  // not needed.  Valued data keeps the product path (a non-finite value would
+  // make 0 * x NaN there, as in the reference).
+  bool zero = !E->ds->has_vals;
+  for (int64_t j = 0; j < p && zero; ++j) zero = beta[j] == 0.0;
+  GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
+  if (zero) {
+    GSS_CUDA(cudaMemsetAsync(E->scratch, 0, E->ds->npad * sizeof(double), s));
+  } else {
     const int rc2 = ensure_csr(E->ds);
     if (rc2) {
       cudaFree(dbeta);
@@ -1124,9 +1146,8 @@ int gss_engine_load_beta(gss_engine* E, const double* beta, int64_t p) {
     E->prm.row_ptr = E->ds->row_ptr;
     E->prm.csr_col = E->ds->csr_col;
     E->prm.csr_val = E->ds->csr_val;
+    GSS_CUDA(launch_spmv_rows(E->prm, dbeta, E->scratch, E->dflag, s));
   }
-  GSS_CUDA(cudaMemsetAsync(E->dflag, 0, sizeof(int), s));
-  GSS_CUDA(launch_spmv_rows(E->prm, dbeta, E->scratch, E->dflag, s));
   int over = 0;
   GSS_CUDA(cudaMemcpyAsync(&over, E->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   GSS_CUDA(cudaStreamSynchronize(s));

@@ -177,6 +177,8 @@ cudaError_t launch_fill_dense(const int64_t* col_ptr, const int32_t* row_idx, co
                               cudaStream_t s);
 cudaError_t launch_colmax(const int64_t* col_ptr, const double* vals, int64_t p,
                           double* colmax, cudaStream_t s);
+// e[i] = 0 if code[i] & kCodeMasked else 1 (engine start, beta = 0)
+cudaError_t launch_init_e(const uint32_t* code, int64_t npad, double* e, cudaStream_t s);
 cudaError_t launch_csr_count(const int32_t* row_idx, int64_t nnz, int64_t* row_cnt,
                              cudaStream_t s);
 cudaError_t launch_csr_fill(const int64_t* col_ptr, const int32_t* row_idx, const double* vals,
