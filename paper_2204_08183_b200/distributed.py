@@ -13,13 +13,18 @@ There is no data-path collective; "scaling" is weak in tasks per GPU.
 from __future__ import annotations
 
 import math
+import sys
 from typing import Callable, List, Optional, Sequence
 
 TaskRunner = Callable[[Sequence[int]], List[Optional[List[float]]]]
 
 
 def _dist():
-    import torch.distributed as dist
+    # no process group can exist unless torch.distributed was imported: a
+    # single-process caller does not pay the (seconds-long) torch import
+    dist = sys.modules.get("torch.distributed")
+    if dist is None:
+        return None, 0, 1
     if dist.is_available() and dist.is_initialized():
         return dist, dist.get_rank(), dist.get_world_size()
     return None, 0, 1
